@@ -1,0 +1,427 @@
+"""Benchmark of the B200 convtact hot path (driver contract: one JSON line on rank 0).
+
+Headline workload (BASELINE.json configs[1], the config the TTC metric is
+quoted on): single-scale TTC in float64 over synthetic approaching-plane
+videos of 64 frames x 256 x 256 (the reference generator's construction,
+seeded, generated on the device).  One step = run_sequence(level=0) over a
+batch of V such videos per GPU (frames resident in HBM, V*33.5 MB >> L2):
+fused moments kernel + solve, every pair of every video.  value = estimates
+(frame pairs) per second over all ranks; scaling is weak (V videos per rank,
+no data-path collective -- videos are independent).
+
+Also reported on the same line:
+  roofline     the fused moments kernel (ttc_moments_kernel), algorithmic
+               bytes = 8*256*256 B per estimate (each frame read once,
+               SURVEY.md 8(d)), timed live with CUDA events on its stream;
+  e2e          the same metric through the public host API
+               (run_sequence_host on pinned numpy frames, H2D of every frame
+               and D2H of every estimate inside the timed region);
+  cpu_baseline the CPU oracle port (C restatement of the reference, OpenMP
+               over pairs) on rank 0, bounded sample;
+  secondary    the other BASELINE configs (conv Gpix/s, multiscale TTC).
+
+--impl reference times the CPU reference restatement (oracle/, all host
+threads) on the same workload and prints the same line with impl=reference.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+H = W = 256
+NFRAMES = 64
+BYTES_PER_EST = 8 * H * W  # each frame read once per estimate
+METRIC = "TTC frames/s (estimates/s), single-scale fp64, 64x256x256 approach videos"
+UNIT = "estimates/s"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def load_ncu_traffic(key):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get(key)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """Polls SM clocks and throttle reasons through NVML during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int, period: float = 0.005):
+        self.index, self.period = index, period
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def dist_setup():
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(local)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def make_videos(V: int, seed0: int = 0):
+    """V cfg2 videos [V, 64, 256, 256] f64 on the device; video v uses seed seed0+v
+    (video 0 is BASELINE config 2 itself: seed 0, FOE centre, t0 = 100)."""
+    import torch
+    import paper_1612_08825_b200 as ct
+    frames = torch.empty((V, NFRAMES, H, W), dtype=torch.float64, device="cuda")
+    mags = [100.0 / (100.0 - t) for t in range(NFRAMES)]
+    for v in range(V):
+        tex = ct.make_texture(W, H, seed0 + v)
+        ct.zoom_frames(tex, (0.5 * W, 0.5 * H), mags, out=frames[v])
+    return frames
+
+
+def cpu_baseline_sample(seconds: float = 10.0):
+    """Oracle port on this host: cfg2 video repeated until ~`seconds` of CPU work."""
+    import oracle
+    f = oracle.generate(W, H, NFRAMES, 100.0, (0.5, 0.5), 0, 0.0)
+    threads = len(os.sched_getaffinity(0))
+    oracle.run_sequence(f[:4], level=0, nthreads=threads)  # warm
+    n_est, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < seconds:
+        oracle.run_sequence(f, level=0, nthreads=threads)
+        n_est += NFRAMES - 1
+    dt = time.perf_counter() - t0
+    return {"value": n_est / dt, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{n_est // (NFRAMES - 1)} x cfg2 video (64x256x256 f64) through oracle.run_sequence, "
+                      f"{dt:.1f} s wall, OpenMP over pairs"}
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    import oracle
+    threads = len(os.sched_getaffinity(0))
+    f = oracle.generate(W, H, NFRAMES, 100.0, (0.5, 0.5), 0, 0.0)
+    per_step = max(1, args.ref_videos)
+    for _ in range(args.warmup):
+        oracle.run_sequence(f, level=0, nthreads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        for _ in range(per_step):
+            oracle.run_sequence(f, level=0, nthreads=threads)
+    dt = time.perf_counter() - t0
+    n = args.steps * per_step * (NFRAMES - 1)
+    value = n / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "cfg2 single-scale TTC fp64, 64x256x256 approach video",
+                   "videos_per_step": per_step, "parallelism": f"cpu x{threads} threads (rank 0 only)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{per_step} cfg2 video(s) per step through the C restatement of the reference "
+                                   f"(oracle/convtact_oracle.c; the reference itself is Python+numba and does not "
+                                   f"travel to the GPU box)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def time_moments_kernel(frames, steps):
+    """Live CUDA-event timing of the dominant kernel launch (ct_ttc_moments on the bench input)."""
+    import torch
+    from paper_1612_08825_b200 import _lib
+    L = _lib.load()
+    V, n, h, w = frames.shape
+    sums = torch.empty((V, n - 1, 11), dtype=torch.float64, device="cuda")
+    nb = L.ct_ttc_moments_workspace_bytes(_lib.CT_F64, V, n, h, w)
+    ws = _lib.workspace(nb, "cuda")
+    st = torch.cuda.current_stream()
+
+    def launch():
+        _lib.check(L.ct_ttc_moments(_lib.CT_F64, _lib.ptr(frames), V, n, h, w, _lib.ptr(sums), _lib.ptr(ws), nb,
+                                    st.cuda_stream))
+
+    for _ in range(3):
+        launch()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(steps):
+        launch()
+    e1.record(st)
+    e1.synchronize()
+    return e0.elapsed_time(e1) / steps * 1e-3  # seconds per launch (moments + its finalize)
+
+
+def secondary_configs(quick: bool):
+    """Other BASELINE configs, each timed with CUDA events (not the headline)."""
+    import torch
+    import paper_1612_08825_b200 as ct
+    out = {}
+    st = torch.cuda.current_stream()
+
+    def timeit(fn, reps):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(reps):
+            fn()
+        e1.record(st)
+        e1.synchronize()
+        return e0.elapsed_time(e1) / reps * 1e-3
+
+    hbm, _ = load_peaks()
+    # cfg1: 2-D FULL fp64 256^2 * 5^2, batch of distinct images (>> L2)
+    B = 512 if quick else 2048
+    s = torch.rand((B, 256, 256), dtype=torch.float64, device="cuda")
+    s[0] = torch.from_numpy(np.random.Generator(np.random.PCG64(0)).random((256, 256)))
+    k = np.random.Generator(np.random.PCG64(1)).standard_normal((5, 5))
+    o = torch.empty((B, 260, 260), dtype=torch.float64, device="cuda")
+    t = timeit(lambda: ct.direct_batch(s, k, out=o), 10)
+    bytes_ = B * 8 * (256 * 256 + 260 * 260)
+    out["cfg1_conv2d_fp64_5x5"] = {"gpix_s": B * 260 * 260 / t / 1e9, "batch": B, "ms_per_launch": t * 1e3,
+                                   "roofline": {"bound": "hbm", "achieved": bytes_ / t / 1e9, "peak": hbm,
+                                                "unit": "GB/s", "frac": bytes_ / t / 1e9 / hbm}}
+    del s, o
+    # cfg3: 3-D FULL fp32 128^3 * 7^3
+    B3 = 8
+    s3 = torch.rand((B3, 128, 128, 128), dtype=torch.float32, device="cuda")
+    k3 = np.random.Generator(np.random.PCG64(1)).standard_normal((7, 7, 7)).astype(np.float32)
+    o3 = torch.empty((B3, 134, 134, 134), dtype=torch.float32, device="cuda")
+    t = timeit(lambda: ct.direct_batch(s3, k3, out=o3), 5)
+    fl = B3 * 2.0 * 128 ** 3 * 343
+    out["cfg3_conv3d_fp32_7^3"] = {"gpix_s": B3 * 134 ** 3 / t / 1e9, "batch": B3, "ms_per_launch": t * 1e3,
+                                   "roofline": {"bound": "fp32", "achieved": fl / t / 1e12, "peak": 69.3,
+                                                "unit": "TFLOP/s", "frac": fl / t / 1e12 / 69.3,
+                                                "peak_note": "FFMA-chain microbenchmark on the box (tools/fp_peak.cu)"}}
+    del s3, o3
+    # cfg4: large-kernel 2-D FULL fp32 2048^2 * 31^2
+    B4 = 2
+    s4 = torch.rand((B4, 2048, 2048), dtype=torch.float32, device="cuda")
+    k4 = np.random.Generator(np.random.PCG64(1)).standard_normal((31, 31)).astype(np.float32)
+    o4 = torch.empty((B4, 2078, 2078), dtype=torch.float32, device="cuda")
+    t = timeit(lambda: ct.direct_batch(s4, k4, out=o4), 5)
+    fl = B4 * 2.0 * 2048 ** 2 * 961
+    out["cfg4_conv2d_fp32_31x31"] = {"gpix_s": B4 * 2078 ** 2 / t / 1e9, "batch": B4, "ms_per_launch": t * 1e3,
+                                     "roofline": {"bound": "fp32", "achieved": fl / t / 1e12, "peak": 69.3,
+                                                  "unit": "TFLOP/s", "frac": fl / t / 1e12 / 69.3,
+                                                  "peak_note": "FFMA-chain microbenchmark on the box (tools/fp_peak.cu)"}}
+    del s4, o4
+    # cfg5: multiscale fp32 1080x1920, max_level=3 (reduced stream: 2 videos x 64 frames in quick mode)
+    nv, nf = (1, 64) if quick else (2, 128)
+    fr = torch.empty((nv, nf, 1080, 1920), dtype=torch.float32, device="cuda")
+    for v in range(nv):
+        ct.approach_stream(nf, 1080, 1920, seed=1000 + v, dtype=torch.float32, out=fr[v])
+    t = timeit(lambda: ct.run_sequence_batch(fr, max_level=3), 3)
+    n_est = nv * (nf - 1)
+    bytes_ = n_est * 4 * 1080 * 1920
+    out["cfg5_multiscale_fp32_1080p"] = {"est_s": n_est / t, "videos": nv, "frames": nf, "ms_per_step": t * 1e3,
+                                         "roofline": {"bound": "hbm", "achieved": bytes_ / t / 1e9, "peak": hbm,
+                                                      "unit": "GB/s", "frac": bytes_ / t / 1e9 / hbm,
+                                                      "note": "whole pipeline (pyramid + 4 moment levels + solve)"}}
+    del fr
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--videos", type=int, default=256, help="cfg2 videos per GPU per step")
+    ap.add_argument("--ref-videos", type=int, default=2, help="videos per step for --impl reference")
+    ap.add_argument("--e2e-videos", type=int, default=32)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--quick", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+
+    import torch
+    import paper_1612_08825_b200 as ct
+
+    V = args.videos
+    frames = make_videos(V, seed0=rank * V)
+    out = torch.empty((V, NFRAMES - 1, 10), dtype=torch.float64, device="cuda")
+    st = torch.cuda.current_stream()
+
+    for _ in range(args.warmup):
+        ct.run_sequence_batch(frames, level=0, out=out)
+    torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        e0.record(st)
+        for _ in range(args.steps):
+            ct.run_sequence_batch(frames, level=0, out=out)
+        e1.record(st)
+        e1.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    dt = max_over_ranks(e0.elapsed_time(e1) * 1e-3, world)
+    n_est = world * V * (NFRAMES - 1) * args.steps
+    value = n_est / dt
+    # launches per step: ttc_moments + moments_finalize + ttc_solve
+    launches = 3 * args.steps
+
+    # sanity: the timed output is the real thing (pair 0 of video 0 is cfg2 pair 0)
+    if rank == 0:
+        ttc0 = float(out[0, 0, 5])
+        assert abs(ttc0 - 97.315722253398093) <= 1e-9 * 97.3, ttc0
+
+    # roofline of the dominant kernel, timed live on its stream
+    t_k = time_moments_kernel(frames, max(5, args.steps))
+    hbm, peak_kind = load_peaks()
+    achieved = V * (NFRAMES - 1) * BYTES_PER_EST / t_k / 1e9
+    traffic = load_ncu_traffic("ttc_moments_kernel<double>/cfg2")
+    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+            "traffic": traffic, "kernel": "ttc_moments_kernel<double> (+ finalize)", "peak_kind": peak_kind,
+            "kernel_ms": t_k * 1e3, "step_ms": dt / args.steps * 1e3,
+            "fp64_pipe": {"dp_ops_per_grid_px": 20, "achieved_tflops": 2 * 20 * V * (NFRAMES - 1) * 255 * 255 / t_k / 1e12 / 2,
+                          "peak_tflops": 32.2, "peak_note": "DFMA-chain microbenchmark on the box (tools/fp_peak.cu)"}}
+
+    # end to end through the public host API: pinned frames in, estimates out
+    Ve = min(args.e2e_videos, V)
+    host = torch.empty((Ve, NFRAMES, H, W), dtype=torch.float64).pin_memory()
+    host.copy_(frames[:Ve])
+    hnp = host.numpy()
+    ct.run_sequence_host(hnp, level=0)
+    torch.cuda.synchronize()
+    barrier(world)
+    e_steps = max(3, args.steps // 4)
+    t0 = time.perf_counter()
+    for _ in range(e_steps):
+        est_h = ct.run_sequence_host(hnp, level=0)
+    torch.cuda.synchronize()
+    e_dt = max_over_ranks((time.perf_counter() - t0) / e_steps, world)
+    assert abs(est_h[0, 0, 5] - 97.315722253398093) <= 1e-9 * 97.3
+    e2e = {"value": world * Ve * (NFRAMES - 1) / e_dt, "unit": UNIT,
+           "h2d_bytes_per_step": Ve * NFRAMES * H * W * 8, "d2h_bytes_per_step": Ve * (NFRAMES - 1) * 10 * 8,
+           "videos_per_step": Ve, "api": "paper_1612_08825_b200.run_sequence_host (ct_run_sequence_host)"}
+    del host
+
+    secondary = None
+    if rank == 0 and not args.no_secondary:
+        try:
+            secondary = secondary_configs(args.quick)
+        except Exception as exc:  # reported, never silently dropped
+            secondary = {"error": repr(exc)}
+    cpu = cpu_baseline_sample(args.cpu_seconds) if (rank == 0 and world == 1) else None
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "cfg2 single-scale TTC fp64: 64-frame 256x256 approach videos (t0=100, FOE centre)",
+                       "videos_per_gpu_per_step": V, "estimates_per_step": world * V * (NFRAMES - 1),
+                       "input_bytes_per_gpu": V * NFRAMES * H * W * 8,
+                       "l2": "inputs larger than L2 (>= 8.6 GB per GPU vs 126 MB)",
+                       "parallelism": f"dp{world} (independent videos per rank)"},
+            "roofline": roof,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "secondary": secondary,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

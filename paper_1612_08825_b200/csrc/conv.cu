@@ -1,0 +1,449 @@
+// Direct n-D correlation / convolution (K1-K4) for sm_100a.
+//
+// Replaces the reference's compiled loops _loops.xcorr_{valid,zpad}_{1,2,3}d
+// and the numpy shift-and-add path for ndim >= 4 (_loops.py:27-208), behind
+// the semantics layer conv._direct (conv.py:133-158).
+//
+// Per-output arithmetic is kept identical to the reference: taps are
+// accumulated from 0.0 in row-major (j0, j1, j2) order with FMA for ranks 1-3
+// (numba fastmath contracts `out += kv * s`), and with a rounded multiply
+// followed by a rounded add for ranks >= 4 (numpy `out += k[idx] * s[win]`).
+// Zero extension adds fma(k, 0, acc) == acc for taps the reference skips, so
+// float64 results are bit-identical to the reference for finite inputs.
+//
+// Two kernels:
+//  * xcorr_tiled<T, NW, VX, TY, TZ>: ranks 1-3.  A CTA stages a signal tile
+//    (with the K-1 halo, zero- or clamp-filled) per input z-slice in shared
+//    memory, each thread owns a TZ x TY x VX register block of outputs (VX
+//    consecutive x, loaded as one 16-byte vector per chunk).  Input rows are
+//    the outer loop so every staged value feeds up to TZ*TY*VX FMAs; kernel
+//    taps live in the kernel-parameter constant bank (uniform operands).
+//    NW (kernel x extent) is a compile-time parameter for the widths below.
+//  * xcorr_generic<T>: any rank <= CT_MAXDIM and any kernel width; one thread
+//    per output, odometer over taps.  Used for ranks >= 4 and widths without
+//    a tiled instantiation.
+#include <string.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace ct {
+namespace {
+
+constexpr int kMaxTapsF64 = 1024;  // 8 KB of kernel parameters
+constexpr int kMaxTapsF32 = 2048;  // 8 KB
+
+template <typename T>
+struct MaxTaps;
+template <>
+struct MaxTaps<double> {
+  static constexpr int value = kMaxTapsF64;
+};
+template <>
+struct MaxTaps<float> {
+  static constexpr int value = kMaxTapsF32;
+};
+
+template <typename T>
+struct TapsParam {
+  T v[MaxTaps<T>::value];
+};
+
+template <typename T, int VX>
+struct VecT;
+template <>
+struct VecT<double, 2> {
+  using type = double2;
+};
+template <>
+struct VecT<float, 4> {
+  using type = float4;
+};
+
+struct TileArgs {
+  const void* s;
+  void* out;
+  int64_t batch;
+  int mz, my, mx;
+  int oz, oy, ox;
+  int nz, ny;
+  int pz, py, px;
+  int boundary;
+  int txn, tyn;  // threads along x, thread rows
+  int tiles_z;   // z tiles per signal
+  int sx, sy;    // staged tile extents (elements)
+};
+
+__device__ __forceinline__ double fmadd(double k, double v, double acc) { return fma(k, v, acc); }
+__device__ __forceinline__ float fmadd(float k, float v, float acc) { return fmaf(k, v, acc); }
+
+template <typename T, int NW, int VX, int TY, int TZ>
+__global__ void __launch_bounds__(256) xcorr_tiled(const TileArgs a,
+                                                   const __grid_constant__ TapsParam<T> taps) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* tile = reinterpret_cast<T*>(smem_raw);
+  using V = typename VecT<T, VX>::type;
+  constexpr int CH = (VX + NW - 1 + VX - 1) / VX;  // vector chunks per input row window
+
+  const int tid = threadIdx.x;
+  const int nthr = blockDim.x;
+  const int tx = tid % a.txn, ty = tid / a.txn;
+  const int BX = a.txn * VX, BY = a.tyn * TY;
+  const int x0 = blockIdx.x * BX, y0 = blockIdx.y * BY;
+  const int ny = a.ny, nz = a.nz;
+  const int64_t plane = (int64_t)a.my * a.mx;
+  const int64_t n_ztiles = a.batch * a.tiles_z;
+
+  for (int64_t bz = blockIdx.z; bz < n_ztiles; bz += gridDim.z) {
+    const int64_t b = bz / a.tiles_z;
+    const int z0 = (int)(bz % a.tiles_z) * TZ;
+    const T* s = reinterpret_cast<const T*>(a.s) + b * (int64_t)a.mz * plane;
+
+    T acc[TZ][TY][VX];
+#pragma unroll
+    for (int i = 0; i < TZ; ++i)
+#pragma unroll
+      for (int j = 0; j < TY; ++j)
+#pragma unroll
+        for (int r = 0; r < VX; ++r) acc[i][j][r] = T(0);
+
+    const int nzin = TZ + nz - 1;
+    for (int izr = 0; izr < nzin; ++izr) {
+      int gz = z0 - a.pz + izr;
+      if (gz < 0 || gz >= a.mz) {
+        if (a.boundary == CT_ZERO) continue;  // all-zero slice: adds nothing
+        gz = gz < 0 ? 0 : a.mz - 1;
+      }
+      __syncthreads();  // previous slice fully consumed
+      {
+        const T* sp = s + gz * plane;
+        const int iy0 = y0 - a.py, ix0 = x0 - a.px;
+        const int total = a.sx * a.sy;
+        for (int idx = tid; idx < total; idx += nthr) {
+          const int r = idx / a.sx, c = idx - r * a.sx;
+          int gy = iy0 + r, gx = ix0 + c;
+          T v = T(0);
+          const bool in = (unsigned)gy < (unsigned)a.my && (unsigned)gx < (unsigned)a.mx;
+          if (in) {
+            v = __ldg(sp + (int64_t)gy * a.mx + gx);
+          } else if (a.boundary == CT_REPLICATE) {
+            gy = min(max(gy, 0), a.my - 1);
+            gx = min(max(gx, 0), a.mx - 1);
+            v = __ldg(sp + (int64_t)gy * a.mx + gx);
+          }
+          tile[idx] = v;
+        }
+      }
+      __syncthreads();
+
+      const int nrows = TY + ny - 1;
+      for (int r = 0; r < nrows; ++r) {
+        // every thread-row window value of this staged input row
+        T v[CH * VX];
+        const T* rowp = tile + (ty * TY + r) * a.sx + tx * VX;
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+          const V q = *reinterpret_cast<const V*>(rowp + c * VX);
+          const T* qp = reinterpret_cast<const T*>(&q);
+#pragma unroll
+          for (int e = 0; e < VX; ++e) v[c * VX + e] = qp[e];
+        }
+#pragma unroll
+        for (int zi = 0; zi < TZ; ++zi) {
+          const int j0 = izr - zi;
+          if (j0 < 0 || j0 >= nz) continue;
+#pragma unroll
+          for (int yi = 0; yi < TY; ++yi) {
+            const int j1 = r - yi;
+            if (j1 < 0 || j1 >= ny) continue;
+            const T* kr = taps.v + (j0 * ny + j1) * NW;
+#pragma unroll
+            for (int j2 = 0; j2 < NW; ++j2) {
+              const T kv = kr[j2];
+#pragma unroll
+              for (int rr = 0; rr < VX; ++rr) acc[zi][yi][rr] = fmadd(kv, v[rr + j2], acc[zi][yi][rr]);
+            }
+          }
+        }
+      }
+    }
+
+    // store the register block
+    T* out = reinterpret_cast<T*>(a.out) + b * (int64_t)a.oz * a.oy * a.ox;
+#pragma unroll
+    for (int zi = 0; zi < TZ; ++zi) {
+      const int z = z0 + zi;
+      if (z >= a.oz) break;
+#pragma unroll
+      for (int yi = 0; yi < TY; ++yi) {
+        const int y = y0 + ty * TY + yi;
+        if (y >= a.oy) break;
+        T* orow = out + ((int64_t)z * a.oy + y) * a.ox;
+        const int x = x0 + tx * VX;
+#pragma unroll
+        for (int rr = 0; rr < VX; ++rr)
+          if (x + rr < a.ox) orow[x + rr] = acc[zi][yi][rr];
+      }
+    }
+  }
+}
+
+struct GenArgs {
+  const void* s;
+  const void* k;
+  void* out;
+  int64_t batch;
+  int ndim;
+  int boundary;
+  int fused;
+  int flip;
+  int64_t ms[CT_MAXDIM], ns[CT_MAXDIM], pl[CT_MAXDIM], os[CT_MAXDIM];
+  int64_t sstr[CT_MAXDIM];
+  int64_t s_elems, o_elems, k_elems;
+};
+
+template <typename T>
+__device__ __forceinline__ T mul_add_rn(T k, T v, T acc);
+template <>
+__device__ __forceinline__ double mul_add_rn(double k, double v, double acc) {
+  return __dadd_rn(acc, __dmul_rn(k, v));
+}
+template <>
+__device__ __forceinline__ float mul_add_rn(float k, float v, float acc) {
+  return __fadd_rn(acc, __fmul_rn(k, v));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) xcorr_generic(const GenArgs a) {
+  const int64_t total = a.batch * a.o_elems;
+  const T* kk = reinterpret_cast<const T*>(a.k);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = i / a.o_elems;
+    int64_t rem = i - b * a.o_elems;
+    int64_t o[CT_MAXDIM];
+    for (int d = a.ndim - 1; d >= 0; --d) {
+      o[d] = rem % a.os[d];
+      rem /= a.os[d];
+    }
+    const T* s = reinterpret_cast<const T*>(a.s) + b * a.s_elems;
+    T acc = T(0);
+    int64_t j[CT_MAXDIM];
+    for (int d = 0; d < a.ndim; ++d) j[d] = 0;
+    for (int64_t t = 0; t < a.k_elems; ++t) {
+      int64_t off = 0;
+      bool in = true;
+      for (int d = 0; d < a.ndim; ++d) {
+        int64_t si = o[d] - a.pl[d] + j[d];
+        if (si < 0 || si >= a.ms[d]) {
+          if (a.boundary == CT_ZERO) {
+            in = false;
+            break;
+          }
+          si = si < 0 ? 0 : a.ms[d] - 1;
+        }
+        off += si * a.sstr[d];
+      }
+      if (in) {
+        const T kv = kk[a.flip ? a.k_elems - 1 - t : t];
+        const T sv = s[off];
+        acc = a.fused ? fmadd(kv, sv, acc) : mul_add_rn(kv, sv, acc);
+      }
+      for (int d = a.ndim - 1; d >= 0; --d) {  // odometer, row-major
+        if (++j[d] < a.ns[d]) break;
+        j[d] = 0;
+      }
+    }
+    reinterpret_cast<T*>(a.out)[i] = acc;
+  }
+}
+
+template <typename T, int NW, int VX, int TY, int TZ>
+int launch_tiled(const TileArgs& a0, const T* k_host_order_taps, int ntaps, cudaStream_t st) {
+  TileArgs a = a0;
+  TapsParam<T> taps;
+  for (int i = 0; i < ntaps; ++i) taps.v[i] = k_host_order_taps[i];
+  const int BX = a.txn * VX, BY = a.tyn * TY;
+  constexpr int CH = (VX + NW - 1 + VX - 1) / VX;
+  a.sx = BX - VX + CH * VX;
+  a.sy = BY + a.ny - 1;
+  const size_t smem = (size_t)a.sx * a.sy * sizeof(T);
+  auto kern = xcorr_tiled<T, NW, VX, TY, TZ>;
+  if (smem > 48 * 1024) CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 grid((unsigned)cdiv(a.ox, BX), (unsigned)cdiv(a.oy, BY),
+            (unsigned)std::min<int64_t>(a.batch * a.tiles_z, 65535));
+  kern<<<grid, a.txn * a.tyn, smem, st>>>(a, taps);
+  return check_launch("xcorr_tiled");
+}
+
+// The tiled kernel takes its taps through the kernel-parameter bank, so they
+// are needed on the host: the caller's host copy is used when given, else the
+// device kernel is copied (a few KB, synchronising the stream).  flip
+// reverses the flat row-major buffer, which is reflect(k) (conv.py:62-64).
+template <typename T>
+int taps_to_host(const void* k, const void* k_host, int64_t n, int flip, T* dst, cudaStream_t st) {
+  T tmp[MaxTaps<T>::value];
+  if (k_host) {
+    memcpy(tmp, k_host, (size_t)n * sizeof(T));
+  } else {
+    CT_CUDA(cudaMemcpyAsync(tmp, k, (size_t)n * sizeof(T), cudaMemcpyDeviceToHost, st));
+    CT_CUDA(cudaStreamSynchronize(st));
+  }
+  for (int64_t i = 0; i < n; ++i) dst[i] = flip ? tmp[n - 1 - i] : tmp[i];
+  return CT_OK;
+}
+
+template <typename T>
+int dispatch(int ndim, const void* s, const int64_t* ms, int64_t batch, const void* k,
+             const void* k_host, const int64_t* ns, const int64_t* pl, const int64_t* os, int boundary, int flip,
+             void* out, cudaStream_t st) {
+  int64_t k_elems = 1, o_elems = 1, s_elems = 1;
+  for (int d = 0; d < ndim; ++d) {
+    k_elems *= ns[d];
+    o_elems *= os[d];
+    s_elems *= ms[d];
+  }
+  if (o_elems == 0 || batch == 0) return CT_OK;
+  const int nw = (int)ns[ndim - 1];
+  const bool tiled_ok = ndim <= 3 && k_elems <= MaxTaps<T>::value && s_elems > 0 &&
+                        (nw == 1 || nw == 2 || nw == 3 || nw == 4 || nw == 5 || nw == 6 ||
+                         nw == 7 || nw == 8 || nw == 9 || nw == 11 || nw == 15 || nw == 31);
+  if (tiled_ok) {
+    // shapes as 3-D (z, y, x)
+    int64_t m3[3] = {1, 1, 1}, n3[3] = {1, 1, 1}, p3[3] = {0, 0, 0}, o3[3] = {1, 1, 1};
+    for (int d = 0; d < ndim; ++d) {
+      m3[3 - ndim + d] = ms[d];
+      n3[3 - ndim + d] = ns[d];
+      p3[3 - ndim + d] = pl[d];
+      o3[3 - ndim + d] = os[d];
+    }
+    for (int d = 0; d < 3; ++d)
+      CT_REQUIRE(m3[d] < (1 << 30) && o3[d] < (1 << 30) && p3[d] < (1 << 30), "extent too large");
+    T taps_host[MaxTaps<T>::value];
+    int rc = taps_to_host<T>(k, k_host, k_elems, flip, taps_host, st);
+    if (rc) return rc;
+    TileArgs a{};
+    a.s = s;
+    a.out = out;
+    a.batch = batch;
+    a.mz = (int)m3[0]; a.my = (int)m3[1]; a.mx = (int)m3[2];
+    a.oz = (int)o3[0]; a.oy = (int)o3[1]; a.ox = (int)o3[2];
+    a.nz = (int)n3[0]; a.ny = (int)n3[1];
+    a.pz = (int)p3[0]; a.py = (int)p3[1]; a.px = (int)p3[2];
+    a.boundary = boundary;
+    constexpr int VX = 16 / sizeof(T);
+    // x threads: cover the output row with as little padding as possible
+    int txn = (int)std::min<int64_t>(32, cdiv(a.ox, VX));
+    const bool is3d = a.oz > 1 || a.nz > 1;
+    if (is3d) {
+      constexpr int TY = 4, TZ = 2;
+      a.txn = txn;
+      a.tyn = std::max(1, std::min<int>(256 / txn, (int)cdiv(a.oy, TY)));
+      a.tiles_z = (int)cdiv(a.oz, TZ);
+      switch (nw) {
+#define CT_CASE(W) case W: return launch_tiled<T, W, VX, TY, TZ>(a, taps_host, (int)k_elems, st);
+        CT_CASE(1) CT_CASE(2) CT_CASE(3) CT_CASE(4) CT_CASE(5) CT_CASE(6) CT_CASE(7) CT_CASE(8)
+        CT_CASE(9) CT_CASE(11) CT_CASE(15) CT_CASE(31)
+#undef CT_CASE
+      }
+    } else {
+      constexpr int TY = 4, TZ = 1;
+      a.txn = txn;
+      a.tyn = std::max(1, std::min<int>(256 / txn, (int)cdiv(a.oy, TY)));
+      a.tiles_z = 1;
+      switch (nw) {
+#define CT_CASE(W) case W: return launch_tiled<T, W, VX, TY, TZ>(a, taps_host, (int)k_elems, st);
+        CT_CASE(1) CT_CASE(2) CT_CASE(3) CT_CASE(4) CT_CASE(5) CT_CASE(6) CT_CASE(7) CT_CASE(8)
+        CT_CASE(9) CT_CASE(11) CT_CASE(15) CT_CASE(31)
+#undef CT_CASE
+      }
+    }
+  }
+  GenArgs g{};
+  g.s = s;
+  g.k = k;
+  g.out = out;
+  g.batch = batch;
+  g.ndim = ndim;
+  g.boundary = boundary;
+  g.fused = ndim <= 3;
+  g.flip = flip;
+  int64_t acc = 1;
+  for (int d = ndim - 1; d >= 0; --d) {
+    g.ms[d] = ms[d];
+    g.ns[d] = ns[d];
+    g.pl[d] = pl[d];
+    g.os[d] = os[d];
+    g.sstr[d] = acc;
+    acc *= ms[d];
+  }
+  g.s_elems = s_elems;
+  g.o_elems = o_elems;
+  g.k_elems = k_elems;
+  const int64_t total = batch * o_elems;
+  const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(total, 256), (int64_t)num_sms() * 32);
+  xcorr_generic<T><<<blocks, 256, 0, st>>>(g);
+  return check_launch("xcorr_generic");
+}
+
+}  // namespace
+}  // namespace ct
+
+using namespace ct;
+
+static int xcorr_entry(int dtype, int ndim, const void* s, const int64_t* s_shape, int64_t batch,
+                       const void* k, const void* k_host, const int64_t* k_shape, const int64_t* pad_left,
+                       const int64_t* out_shape, int boundary, int flip, void* out, void* stream) {
+  CT_REQUIRE(dtype == CT_F64 || dtype == CT_F32, "dtype must be CT_F64 or CT_F32");
+  CT_REQUIRE(ndim >= 1 && ndim <= CT_MAXDIM, "ndim %d outside 1..%d", ndim, (int)CT_MAXDIM);
+  CT_REQUIRE(boundary == CT_ZERO || boundary == CT_REPLICATE, "bad boundary");
+  CT_REQUIRE(batch >= 0, "negative batch");
+  for (int d = 0; d < ndim; ++d) {
+    CT_REQUIRE(s_shape[d] >= 0 && k_shape[d] >= 1 && out_shape[d] >= 0 && pad_left[d] >= 0,
+               "bad extents on axis %d", d);
+    CT_REQUIRE(boundary == CT_ZERO || s_shape[d] >= 1, "replicate needs a non-empty signal");
+  }
+  cudaStream_t st = as_stream(stream);
+  if (dtype == CT_F64)
+    return dispatch<double>(ndim, s, s_shape, batch, k, k_host, k_shape, pad_left, out_shape, boundary, flip, out, st);
+  return dispatch<float>(ndim, s, s_shape, batch, k, k_host, k_shape, pad_left, out_shape, boundary, flip, out, st);
+}
+
+extern "C" int ct_xcorr_nd(int dtype, int ndim, const void* s, const int64_t* s_shape,
+                           int64_t batch, const void* k, const void* k_host, const int64_t* k_shape,
+                           const int64_t* pad_left, const int64_t* out_shape, int boundary,
+                           void* out, void* stream) {
+  clear_error();
+  return xcorr_entry(dtype, ndim, s, s_shape, batch, k, k_host, k_shape, pad_left, out_shape, boundary, 0, out,
+                     stream);
+}
+
+extern "C" int ct_direct(int dtype, int ndim, const void* s, const int64_t* s_shape, int64_t batch,
+                         const void* k, const void* k_host, const int64_t* k_shape, int shape, int boundary, int flip,
+                         void* out, void* stream) {
+  clear_error();
+  CT_REQUIRE(ndim >= 1 && ndim <= CT_MAXDIM, "zero-rank tensors not supported");
+  CT_REQUIRE(shape == CT_FULL || shape == CT_SAME || shape == CT_VALID, "bad shape");
+  int64_t pl[CT_MAXDIM], os[CT_MAXDIM];
+  for (int d = 0; d < ndim; ++d) {
+    const int64_t m = s_shape[d], n = k_shape[d];
+    CT_REQUIRE(n >= 1 && m >= 0, "bad extents on axis %d", d);
+    if (shape == CT_FULL) {  // conv.py:142-145
+      pl[d] = n - 1;
+      os[d] = m + n - 1;
+    } else if (shape == CT_SAME) {  // conv.py:146-150, _same_pads conv.py:115-117
+      pl[d] = (n - 1) - (n - 1) / 2;
+      os[d] = m;
+    } else {  // conv.py:139-141, _check_valid conv.py:93-98
+      CT_REQUIRE(m >= n, "VALID needs signal >= kernel on every axis, axis %d has %lld < %lld", d,
+                 (long long)m, (long long)n);
+      pl[d] = 0;
+      os[d] = m - n + 1;
+    }
+  }
+  // The boundary policy only matters where SAME reads outside the signal
+  // (conv.py:146-150); FULL and VALID always zero-extend.
+  const int bnd = shape == CT_SAME ? boundary : CT_ZERO;
+  return xcorr_entry(dtype, ndim, s, s_shape, batch, k, k_host, k_shape, pl, os, bnd, flip ? 1 : 0, out, stream);
+}

@@ -1,0 +1,911 @@
+// Time-to-contact hot path (K5-K7) for sm_100a.
+//
+// Reference (paths under /root/reference/pkg/src/convtact):
+//   derivatives_3d      ttc.py:82-91   (2x2x2 quarter-weight stencils ttc.py:28-31)
+//   radial_gradient     ttc.py:94-99
+//   build_normal_system ttc.py:102-120
+//   _ldlt_solve / solve_ttc  ttc.py:123-184
+//   downsample          ttc.py:187-204
+//   _estimate_at / estimate_fixed / estimate_multiscale / run_sequence  ttc.py:207-305
+//
+// The fused kernel (ttc_moments_kernel) is the product's hot loop: one CTA
+// owns a band of BR grid rows x 255 grid columns of one video and walks a
+// chunk of consecutive frames.  Frame bands arrive by TMA into a 3-deep ring
+// of shared-memory buffers (mbarrier-tracked), so every frame is read from
+// HBM once per band and the two frames of pair t are both resident; no
+// derivative field is ever written.  Per pixel it evaluates the cube
+// stencils from time sums P = a + b and differences D = b - a (4x-scaled:
+// Ex' = dP_y + dP_y+1, Ey' = hP_y+1 - hP_y, Et' = sD_y + sD_y+1), and
+// accumulates per-column moments with G folded out algebraically
+// (G = xc*Ex + yc*Ey; with H = yc*Ey the G moments are xc-weighted column
+// sums plus sums of Ex*H, Ey*H, H*Et, H*H).  Per pair the CTA reduces its
+// ten sums (warp shuffle, then shared memory) into a per-band partial; a
+// second kernel adds the partials in a fixed order, so results do not depend
+// on scheduling (bit-reproducible run to run and across shard counts).
+#include <math.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "tma.cuh"
+
+namespace ct {
+namespace {
+
+template <typename T>
+struct AccT;
+template <>
+struct AccT<double> {
+  using type = double;
+};
+template <>
+struct AccT<float> {
+  using type = float;
+};
+
+constexpr int kBoxCols = 256;     // frame columns per tile (TMA box inner extent)
+constexpr int kTileGridCols = 255;  // grid columns produced per tile
+constexpr int kMomThreads = 128;  // 2 grid columns per thread
+
+struct MomentArgs {
+  const void* frames;
+  double* partials;  // [n_videos][n_pairs][units][10]
+  int64_t n_videos;
+  int n_frames;
+  int h, w, gh, gw, border;
+  int band_rows;
+  int n_bands, n_ctiles, units;
+  int chunk;  // pairs per CTA
+  int use_tma;
+};
+
+template <typename T>
+__host__ __device__ constexpr size_t band_buf_elems(int band_rows) {
+  // rows x 256 columns, +8 elements so the last thread's right-neighbour
+  // vector read stays inside the buffer (those lanes are masked)
+  return (size_t)(band_rows + 1) * kBoxCols + 8;
+}
+
+template <typename T>
+__host__ __device__ size_t band_buf_bytes(int band_rows) {
+  return (band_buf_elems<T>(band_rows) * sizeof(T) + 127) & ~size_t(127);
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kMomThreads) ttc_moments_kernel(const MomentArgs a,
+                                                                   const __grid_constant__ CUtensorMap tmap) {
+  using ACC = typename AccT<T>::type;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int BR = a.band_rows;
+  const size_t bbytes = band_buf_bytes<T>(BR);
+  T* bufs[3] = {reinterpret_cast<T*>(smem), reinterpret_cast<T*>(smem + bbytes),
+                reinterpret_cast<T*>(smem + 2 * bbytes)};
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 3 * bbytes);
+  double* red = reinterpret_cast<double*>(smem + 3 * bbytes + 64);  // [2][4 warps][10]
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int unit = blockIdx.x;
+  const int band = unit / a.n_ctiles, ctile = unit - band * a.n_ctiles;
+  const int gy0 = band * BR;                 // first grid row (== first frame row) of the band
+  const int cx0 = ctile * kTileGridCols;      // first grid column (== first frame column)
+  const int64_t v = blockIdx.z;
+  const int n_pairs = a.n_frames - 1;
+  const int p0 = blockIdx.y * a.chunk;
+  const int p1 = min(p0 + a.chunk, n_pairs);  // pairs [p0, p1) -> frames p0..p1
+  if (p0 >= p1) return;
+  const int nload = p1 - p0 + 1;
+  const uint32_t box_bytes = (uint32_t)((BR + 1) * kBoxCols * sizeof(T));
+
+  // this thread's two grid columns (local 2*tid, 2*tid+1)
+  const int lc = 2 * tid;
+  const int gxa = cx0 + lc, gxb = gxa + 1;
+  const bool ina = lc < kTileGridCols && gxa >= a.border && gxa < a.gw - a.border;
+  const bool inb = lc + 1 < kTileGridCols && gxb >= a.border && gxb < a.gw - a.border;
+  const ACC xa = (ACC)((double)gxa - (double)(a.gw - 1) / 2.0);
+  const ACC xb = (ACC)((double)gxb - (double)(a.gw - 1) / 2.0);
+  const double ycen = (double)(a.gh - 1) / 2.0;
+  const int64_t row0 = (v * a.n_frames) * (int64_t)a.h + gy0;  // frame p's band row = row0 + p*h
+
+  auto issue = [&](int f) {  // frame p0+f -> buffer f%3
+    T* dst = bufs[f % 3];
+    if (a.use_tma) {
+      if (tid == 0) {
+        mbar_arrive_expect_tx(&bars[f % 3], box_bytes);
+        tma_load_2d(dst, &tmap, &bars[f % 3], cx0, (int)(row0 + (int64_t)(p0 + f) * a.h));
+      }
+    } else {
+      const T* src = reinterpret_cast<const T*>(a.frames) + (row0 + (int64_t)(p0 + f) * a.h) * a.w;
+      const int64_t rows_left = (int64_t)a.n_videos * a.n_frames * a.h - (row0 + (int64_t)(p0 + f) * a.h);
+      for (int idx = tid; idx < (BR + 1) * kBoxCols; idx += kMomThreads) {
+        const int r = idx / kBoxCols, c = idx - r * kBoxCols;
+        T val = T(0);
+        if (r < rows_left && cx0 + c < a.w) val = src[(int64_t)r * a.w + cx0 + c];
+        dst[idx] = val;
+      }
+    }
+  };
+
+  if (a.use_tma) {
+    if (tid == 0) {
+      for (int i = 0; i < 3; ++i) mbar_init(&bars[i], 1);
+      mbar_fence_init();
+    }
+    __syncthreads();
+    for (int f = 0; f < min(3, nload); ++f) issue(f);
+  } else {
+    issue(0);
+    issue(1);
+    __syncthreads();
+  }
+
+  for (int i = 0; i < p1 - p0; ++i) {
+    const int p = p0 + i;
+    if (a.use_tma) {
+      mbar_wait(&bars[i % 3], (uint32_t)((i / 3) & 1));
+      mbar_wait(&bars[(i + 1) % 3], (uint32_t)(((i + 1) / 3) & 1));
+    }
+    const T* A = bufs[i % 3];
+    const T* B = bufs[(i + 1) % 3];
+
+    // per-column accumulators: S1..S6 = Ex^2 ExEy Ey^2 ExEt EyEt Et^2, U1..U4 = ExH EyH HEt HH
+    ACC s[2][10];
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int q = 0; q < 10; ++q) s[c][q] = ACC(0);
+
+    ACC hP[2], dP[2], sD[2];
+    {
+      // frame row 0 of the band
+      const T* ra = A + lc;
+      const T* rb = B + lc;
+      ACC pa[3], pd[3];
+#pragma unroll
+      for (int e = 0; e < 3; ++e) {
+        const ACC x0 = (ACC)ra[e], x1 = (ACC)rb[e];
+        pa[e] = x0 + x1;
+        pd[e] = x1 - x0;
+      }
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        hP[c] = pa[c] + pa[c + 1];
+        dP[c] = pa[c + 1] - pa[c];
+        sD[c] = pd[c] + pd[c + 1];
+      }
+    }
+    const int r_end = min(BR, a.gh - a.border - gy0);  // last grid row (exclusive, band-local) + 1
+    const int r_beg = max(1, a.border - gy0 + 1);       // frame row index whose grid row is >= border
+#pragma unroll 2
+    for (int r = 1; r <= BR; ++r) {
+      const T* ra = A + r * kBoxCols + lc;
+      const T* rb = B + r * kBoxCols + lc;
+      ACC pa[3], pd[3];
+#pragma unroll
+      for (int e = 0; e < 3; ++e) {
+        const ACC x0 = (ACC)ra[e], x1 = (ACC)rb[e];
+        pa[e] = x0 + x1;
+        pd[e] = x1 - x0;
+      }
+      ACC nhP[2], ndP[2], nsD[2];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        nhP[c] = pa[c] + pa[c + 1];
+        ndP[c] = pa[c + 1] - pa[c];
+        nsD[c] = pd[c] + pd[c + 1];
+      }
+      // grid row gy = gy0 + r - 1
+      if (r >= r_beg && r <= r_end) {
+        const ACC yc = (ACC)((double)(gy0 + r - 1) - ycen);
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const ACC ex = dP[c] + ndP[c];
+          const ACC ey = nhP[c] - hP[c];
+          const ACC et = sD[c] + nsD[c];
+          const ACC hh = yc * ey;
+          s[c][0] = fma(ex, ex, s[c][0]);
+          s[c][1] = fma(ex, ey, s[c][1]);
+          s[c][2] = fma(ey, ey, s[c][2]);
+          s[c][3] = fma(ex, et, s[c][3]);
+          s[c][4] = fma(ey, et, s[c][4]);
+          s[c][5] = fma(et, et, s[c][5]);
+          s[c][6] = fma(ex, hh, s[c][6]);
+          s[c][7] = fma(ey, hh, s[c][7]);
+          s[c][8] = fma(hh, et, s[c][8]);
+          s[c][9] = fma(hh, hh, s[c][9]);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        hP[c] = nhP[c];
+        dP[c] = ndP[c];
+        sD[c] = nsD[c];
+      }
+    }
+
+    // combine the columns: ten sums in the order m00 m01 m02 m11 m12 m22 r0 r1 r2 et2
+    double out[10];
+#pragma unroll
+    for (int q = 0; q < 10; ++q) out[q] = 0.0;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const bool on = c == 0 ? ina : inb;
+      if (!on) continue;
+      const double xc = (double)(c == 0 ? xa : xb);
+      const double S1 = s[c][0], S2 = s[c][1], S3 = s[c][2], S4 = s[c][3], S5 = s[c][4], S6 = s[c][5];
+      const double U1 = s[c][6], U2 = s[c][7], U3 = s[c][8], U4 = s[c][9];
+      out[0] += S1;                                   // sum Ex^2
+      out[1] += S2;                                   // sum Ex Ey
+      out[2] += fma(xc, S1, U1);                      // sum Ex G
+      out[3] += S3;                                   // sum Ey^2
+      out[4] += fma(xc, S2, U2);                      // sum Ey G
+      out[5] += fma(xc * xc, S1, fma(2.0 * xc, U1, U4));  // sum G^2
+      out[6] += S4;                                   // sum Ex Et
+      out[7] += S5;                                   // sum Ey Et
+      out[8] += fma(xc, S4, U3);                      // sum G Et
+      out[9] += S6;                                   // sum Et^2
+    }
+#pragma unroll
+    for (int q = 0; q < 10; ++q) out[q] = warp_sum(out[q]);
+    double* rb = red + (i & 1) * 40;
+    if (lane == 0) {
+#pragma unroll
+      for (int q = 0; q < 10; ++q) rb[warp * 10 + q] = out[q];
+    }
+    __syncthreads();  // red written; buffers of frame p0+i fully consumed
+    if (a.use_tma) {
+      if (i + 3 < nload) {
+        if (tid == 0) fence_proxy_async_smem();
+        issue(i + 3);
+      }
+    } else if (i + 2 < nload) {
+      issue(i + 2);  // buffer (i+2)%3 last held frame p0+i-1
+    }
+    if (tid < 10) {
+      const double t = ((rb[tid] + rb[10 + tid]) + (rb[20 + tid] + rb[30 + tid])) * 0.0625;
+      // rhs entries are negated sums (ttc.py:119)
+      a.partials[((v * n_pairs + p) * a.units + unit) * 10 + tid] = (tid >= 6 && tid <= 8) ? -t : t;
+    }
+    if (!a.use_tma) __syncthreads();
+  }
+}
+
+__global__ void moments_finalize_kernel(const double* partials, int64_t n_sys, int units, double count,
+                                        double* sums) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n_sys * 11) return;
+  const int64_t sys = i / 11;
+  const int q = (int)(i - sys * 11);
+  if (q == 10) {
+    sums[i] = count;
+    return;
+  }
+  const double* p = partials + sys * units * 10 + q;
+  double acc = 0.0;
+  for (int u = 0; u < units; ++u) acc += p[(int64_t)u * 10];
+  sums[i] = acc;
+}
+
+// ------------------------------------------------------------ fields ------
+
+template <typename T>
+__device__ __forceinline__ T fmx(T a, T b, T c);
+template <>
+__device__ __forceinline__ double fmx(double a, double b, double c) {
+  return fma(a, b, c);
+}
+template <>
+__device__ __forceinline__ float fmx(float a, float b, float c) {
+  return fmaf(a, b, c);
+}
+
+// derivatives_3d: VALID 3-D correlation of the stacked pair with _DX/_DY/_DT,
+// taps in [t][y][x] order accumulated with FMA from 0 (bit-identical to the
+// reference in float64).
+template <typename T>
+__global__ void deriv_fields_kernel(const T* __restrict__ f0, const T* __restrict__ f1, int h, int w,
+                                    T* ex, T* ey, T* et) {
+  const int gw = w - 1, gh = h - 1;
+  const int64_t n = (int64_t)gh * gw;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int y = (int)(i / gw), x = (int)(i - (int64_t)y * gw);
+    const T v[8] = {f0[(int64_t)y * w + x], f0[(int64_t)y * w + x + 1], f0[(int64_t)(y + 1) * w + x],
+                    f0[(int64_t)(y + 1) * w + x + 1], f1[(int64_t)y * w + x], f1[(int64_t)y * w + x + 1],
+                    f1[(int64_t)(y + 1) * w + x], f1[(int64_t)(y + 1) * w + x + 1]};
+    const T q = T(0.25), m = T(-0.25);
+    T sx = T(0), sy = T(0), st = T(0);
+    const T kx[8] = {m, q, m, q, m, q, m, q};
+    const T ky[8] = {m, m, q, q, m, m, q, q};
+    const T kt[8] = {m, m, m, m, q, q, q, q};
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      sx = fmx(kx[j], v[j], sx);
+      sy = fmx(ky[j], v[j], sy);
+      st = fmx(kt[j], v[j], st);
+    }
+    ex[i] = sx;
+    ey[i] = sy;
+    et[i] = st;
+  }
+}
+
+template <typename T>
+__global__ void radial_gradient_kernel(const T* __restrict__ ex, const T* __restrict__ ey, int gh, int gw,
+                                       T* g) {
+  const int64_t n = (int64_t)gh * gw;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int y = (int)(i / gw), x = (int)(i - (int64_t)y * gw);
+    // xc[None,:]*ex + yc[:,None]*ey, evaluated op by op like numpy (ttc.py:97-99)
+    const double xc = (double)x - (double)(gw - 1) / 2.0;
+    const double yc = (double)y - (double)(gh - 1) / 2.0;
+    const double pr = __dmul_rn(xc, (double)ex[i]);
+    const double qr = __dmul_rn(yc, (double)ey[i]);
+    g[i] = (T)__dadd_rn(pr, qr);
+  }
+}
+
+constexpr int kNsBlocks = 296;
+constexpr int kNsThreads = 256;
+
+template <typename T>
+__global__ void __launch_bounds__(kNsThreads) normal_system_kernel(const T* ex, const T* ey, const T* g,
+                                                                   const T* et, int gh, int gw, int border,
+                                                                   double* partials) {
+  const int iw = gw - 2 * border, ih = gh - 2 * border;
+  const int64_t n = (int64_t)iw * ih;
+  double acc[10];
+#pragma unroll
+  for (int q = 0; q < 10; ++q) acc[q] = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int y = (int)(i / iw) + border, x = (int)(i % iw) + border;
+    const int64_t o = (int64_t)y * gw + x;
+    const double vx = ex[o], vy = ey[o], vg = g[o], vt = et[o];
+    acc[0] += vx * vx;
+    acc[1] += vx * vy;
+    acc[2] += vx * vg;
+    acc[3] += vy * vy;
+    acc[4] += vy * vg;
+    acc[5] += vg * vg;
+    acc[6] += vx * vt;
+    acc[7] += vy * vt;
+    acc[8] += vg * vt;
+    acc[9] += vt * vt;
+  }
+  __shared__ double red[kNsThreads / 32][10];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < 10; ++q) {
+    const double s = warp_sum(acc[q]);
+    if (lane == 0) red[warp][q] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < 10) {
+    double s = 0.0;
+    for (int w2 = 0; w2 < kNsThreads / 32; ++w2) s += red[w2][threadIdx.x];
+    partials[blockIdx.x * 10 + threadIdx.x] = (threadIdx.x >= 6 && threadIdx.x <= 8) ? -s : s;
+  }
+}
+
+// ------------------------------------------------------------- solve ------
+
+// _ldlt_solve + solve_ttc (ttc.py:123-184) and the FOE scaling of
+// _estimate_at (ttc.py:219-225).  Evaluated op by op (no contraction) like
+// the reference's float64 scalar code; v @ rhs is numpy's FMA-chain dot.
+__device__ void solve_one(const double* sm, double c_min, int level, double* e) {
+  const double m00 = sm[0], m01 = sm[1], m02 = sm[2], m11 = sm[3], m12 = sm[4], m22 = sm[5];
+  const double r0 = sm[6], r1 = sm[7], r2 = sm[8], et2 = sm[9], count = sm[10];
+  double maxdiag = m00;
+  if (m11 > maxdiag) maxdiag = m11;
+  if (m22 > maxdiag) maxdiag = m22;
+  bool degenerate = false;
+  double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+  if (maxdiag <= 0.0) {
+    degenerate = true;
+  } else {
+    const double tol = __dmul_rn(1e-10, maxdiag);
+    const double d0 = m00;
+    if (d0 < tol) {
+      degenerate = true;
+    } else {
+      const double l10 = __ddiv_rn(m01, d0);
+      const double l20 = __ddiv_rn(m02, d0);
+      const double d1 = __dsub_rn(m11, __dmul_rn(__dmul_rn(l10, l10), d0));
+      if (d1 < tol) {
+        degenerate = true;
+      } else {
+        const double l21 = __ddiv_rn(__dsub_rn(m12, __dmul_rn(__dmul_rn(l20, l10), d0)), d1);
+        const double d2 = __dsub_rn(__dsub_rn(m22, __dmul_rn(__dmul_rn(l20, l20), d0)),
+                                    __dmul_rn(__dmul_rn(l21, l21), d1));
+        if (d2 < tol) {
+          degenerate = true;
+        } else {
+          const double z0 = r0;
+          const double z1 = __dsub_rn(r1, __dmul_rn(l10, z0));
+          const double z2 = __dsub_rn(__dsub_rn(r2, __dmul_rn(l20, z0)), __dmul_rn(l21, z1));
+          const double y0 = __ddiv_rn(z0, d0), y1 = __ddiv_rn(z1, d1), y2 = __ddiv_rn(z2, d2);
+          v2 = y2;
+          v1 = __dsub_rn(y1, __dmul_rn(l21, v2));
+          v0 = __dsub_rn(__dsub_rn(y0, __dmul_rn(l10, v1)), __dmul_rn(l20, v2));
+        }
+      }
+    }
+  }
+  const double scale = ldexp(1.0, level);
+  if (degenerate) {
+    const double nan = __longlong_as_double(0x7ff8000000000000ll);
+    e[0] = e[1] = e[2] = e[3] = e[4] = e[5] = nan;
+    e[6] = count != 0.0 ? __ddiv_rn(et2, count) : nan;
+    e[7] = __longlong_as_double(0x7ff0000000000000ll);
+    e[8] = (double)level;
+    e[9] = 1.0;
+    return;
+  }
+  const double vr = fma(v2, r2, fma(v1, r1, __dmul_rn(v0, r0)));
+  double j = __dsub_rn(et2, vr);
+  if (0.0 > j) j = 0.0;
+  e[0] = v0;
+  e[1] = v1;
+  e[2] = v2;
+  e[6] = __ddiv_rn(j, count);
+  e[7] = et2 > 0.0 ? __ddiv_rn(j, et2) : __longlong_as_double(0x7ff0000000000000ll);
+  if (fabs(v2) < c_min) {
+    const double nan = __longlong_as_double(0x7ff8000000000000ll);
+    e[3] = nan;
+    e[4] = nan;
+    e[5] = __longlong_as_double(0x7ff0000000000000ll);
+  } else {
+    e[3] = __dmul_rn(__ddiv_rn(-v0, v2), scale);
+    e[4] = __dmul_rn(__ddiv_rn(-v1, v2), scale);
+    e[5] = __ddiv_rn(1.0, v2);
+  }
+  e[8] = (double)level;
+  e[9] = 0.0;
+}
+
+__global__ void ttc_solve_kernel(const double* sums, int64_t count, double c_min, int level, double* est,
+                                 int64_t est_stride) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  solve_one(sums + i * 11, c_min, level, est + i * est_stride);
+}
+
+// estimate_multiscale's greedy walk (ttc.py:264-279) over levels computed
+// up front; identical selection because level l is only visited when every
+// earlier level improved.
+__global__ void multiscale_select_kernel(const double* est_levels, int64_t count, int n_levels, double* best) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const double* e = est_levels + i * n_levels * 10;
+  double* o = best + i * 10;
+  if (n_levels <= 0) {
+    const double nan = __longlong_as_double(0x7ff8000000000000ll);
+    for (int q = 0; q < 10; ++q) o[q] = nan;
+    o[8] = -1.0;
+    return;
+  }
+  int b = 0;
+  double prev = 0.0;
+  for (int l = 0; l < n_levels; ++l) {
+    const double mf = e[l * 10 + 7];
+    if (l > 0 && mf < e[b * 10 + 7]) b = l;
+    if (l > 0 && !(mf < prev * (1.0 - 1e-3))) break;
+    prev = mf;
+  }
+  for (int q = 0; q < 10; ++q) o[q] = e[b * 10 + q];
+}
+
+// ------------------------------------------------------------- pyramid ----
+
+constexpr int kPyTile = 32;
+
+// downsample (ttc.py:187-204): dec = 0.25*(((f00+f01)+f10)+f11) on the even
+// crop, then the 5x5 binomial over the edge-padded dec, taps row-major with
+// FMA (bit-identical to the reference in float64).
+template <typename T>
+__global__ void __launch_bounds__(256) pyramid_down_kernel(const T* __restrict__ in, int64_t n_images, int h,
+                                                           int w, T* __restrict__ out) {
+  __shared__ T dec[kPyTile + 4][kPyTile + 4 + 1];
+  const int dh = h / 2, dw = w / 2;
+  const int tiles_x = (dw + kPyTile - 1) / kPyTile;
+  const int ty0 = (blockIdx.x / tiles_x) * kPyTile, tx0 = (blockIdx.x % tiles_x) * kPyTile;
+  const T b5[5] = {T(1.0 / 16.0), T(4.0 / 16.0), T(6.0 / 16.0), T(4.0 / 16.0), T(1.0 / 16.0)};
+  for (int64_t img = blockIdx.y; img < n_images; img += gridDim.y) {
+    const T* src = in + img * (int64_t)h * w;
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < (kPyTile + 4) * (kPyTile + 4); idx += blockDim.x) {
+      const int r = idx / (kPyTile + 4), c = idx % (kPyTile + 4);
+      const int yy = min(max(ty0 + r - 2, 0), dh - 1), xx = min(max(tx0 + c - 2, 0), dw - 1);
+      const T* p0 = src + (int64_t)(2 * yy) * w + 2 * xx;
+      const T* p1 = p0 + w;
+      T s;
+      if constexpr (sizeof(T) == 8) {
+        s = __dmul_rn(0.25, __dadd_rn(__dadd_rn(__dadd_rn(p0[0], p0[1]), p1[0]), p1[1]));
+      } else {
+        s = __fmul_rn(0.25f, __fadd_rn(__fadd_rn(__fadd_rn(p0[0], p0[1]), p1[0]), p1[1]));
+      }
+      dec[r][c] = s;
+    }
+    __syncthreads();
+    T* dst = out + img * (int64_t)dh * dw;
+    for (int idx = threadIdx.x; idx < kPyTile * kPyTile; idx += blockDim.x) {
+      const int r = idx / kPyTile, c = idx % kPyTile;
+      const int y = ty0 + r, x = tx0 + c;
+      if (y >= dh || x >= dw) continue;
+      T acc = T(0);
+#pragma unroll
+      for (int j0 = 0; j0 < 5; ++j0)
+#pragma unroll
+        for (int j1 = 0; j1 < 5; ++j1) acc = fmx(b5[j0] * b5[j1], dec[r + j0][c + j1], acc);
+      dst[(int64_t)y * dw + x] = acc;
+    }
+  }
+}
+
+// ------------------------------------------------------------- host -------
+
+template <typename T>
+int band_rows_for() {
+  return sizeof(T) == 8 ? 16 : 32;
+}
+
+template <typename T>
+size_t moments_smem_bytes(int br) {
+  return 3 * band_buf_bytes<T>(br) + 64 + 2 * 40 * sizeof(double);
+}
+
+struct MomentPlan {
+  int band_rows, n_bands, n_ctiles, units, chunk, n_chunks;
+};
+
+template <typename T>
+MomentPlan plan_moments(int64_t n_videos, int n_frames, int h, int w) {
+  MomentPlan p{};
+  p.band_rows = band_rows_for<T>();
+  const int gh = h - 1, gw = w - 1;
+  p.n_bands = (gh + p.band_rows - 1) / p.band_rows;
+  p.n_ctiles = (gw + kTileGridCols - 1) / kTileGridCols;
+  p.units = p.n_bands * p.n_ctiles;
+  const int n_pairs = n_frames - 1;
+  // enough CTAs for ~4 waves at 2 CTAs/SM, but at least 8 pairs per CTA so
+  // the one-frame halo of each time chunk stays a small overhead
+  const int64_t target = (int64_t)num_sms() * 2 * 4;
+  const int64_t per_chunk = std::max<int64_t>(1, (int64_t)p.units * n_videos);
+  int64_t chunks = std::max<int64_t>(1, (target + per_chunk - 1) / per_chunk);
+  chunks = std::min<int64_t>(chunks, std::max(1, n_pairs / 8));
+  chunks = std::max<int64_t>(1, std::min<int64_t>(chunks, n_pairs));
+  p.chunk = (int)((n_pairs + chunks - 1) / chunks);
+  p.n_chunks = (n_pairs + p.chunk - 1) / p.chunk;
+  return p;
+}
+
+template <typename T>
+size_t moments_ws_bytes(int64_t n_videos, int n_frames, int h, int w) {
+  if (n_frames < 2 || h < 2 || w < 2) return 0;
+  MomentPlan p = plan_moments<T>(n_videos, n_frames, h, w);
+  return (size_t)n_videos * (n_frames - 1) * p.units * 10 * sizeof(double);
+}
+
+template <typename T>
+int launch_moments(const T* frames, int64_t n_videos, int n_frames, int h, int w, int border, double* sums,
+                   void* ws, size_t ws_bytes, cudaStream_t st) {
+  const int n_pairs = n_frames - 1;
+  if (n_pairs <= 0 || n_videos == 0) return CT_OK;
+  MomentPlan p = plan_moments<T>(n_videos, n_frames, h, w);
+  const size_t need = moments_ws_bytes<T>(n_videos, n_frames, h, w);
+  CT_REQUIRE(ws != nullptr && ws_bytes >= need, "moments workspace too small (%zu < %zu)", ws_bytes, need);
+  MomentArgs a{};
+  a.frames = frames;
+  a.partials = reinterpret_cast<double*>(ws);
+  a.n_videos = n_videos;
+  a.n_frames = n_frames;
+  a.h = h;
+  a.w = w;
+  a.gh = h - 1;
+  a.gw = w - 1;
+  a.border = border;
+  a.band_rows = p.band_rows;
+  a.n_bands = p.n_bands;
+  a.n_ctiles = p.n_ctiles;
+  a.units = p.units;
+  a.chunk = p.chunk;
+  CUtensorMap tmap;
+  memset(&tmap, 0, sizeof(tmap));
+  a.use_tma = encode_tmap_2d(&tmap, frames, sizeof(T), (uint64_t)w, (uint64_t)(n_videos * n_frames * (int64_t)h),
+                             kBoxCols, p.band_rows + 1)
+                  ? 1
+                  : 0;
+  const size_t smem = moments_smem_bytes<T>(p.band_rows);
+  auto kern = ttc_moments_kernel<T>;
+  CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CT_REQUIRE(n_videos <= 65535 && p.n_chunks <= 65535, "too many videos/chunks for one launch");
+  dim3 grid((unsigned)p.units, (unsigned)p.n_chunks, (unsigned)n_videos);
+  kern<<<grid, kMomThreads, smem, st>>>(a, tmap);
+  int rc = check_launch("ttc_moments");
+  if (rc) return rc;
+  const int64_t n_sys = n_videos * n_pairs;
+  const double count = (double)(h - 1 - 2 * border) * (double)(w - 1 - 2 * border);
+  moments_finalize_kernel<<<(unsigned)cdiv(n_sys * 11, 256), 256, 0, st>>>(a.partials, n_sys, p.units, count, sums);
+  return check_launch("moments_finalize");
+}
+
+template <typename T>
+int launch_pyramid(const T* in, int64_t n_images, int h, int w, T* out, cudaStream_t st) {
+  const int dh = h / 2, dw = w / 2;
+  if (n_images == 0 || dh == 0 || dw == 0) return CT_OK;
+  const int tiles = ((dh + kPyTile - 1) / kPyTile) * ((dw + kPyTile - 1) / kPyTile);
+  dim3 grid((unsigned)tiles, (unsigned)std::min<int64_t>(n_images, 65535));
+  pyramid_down_kernel<T><<<grid, 256, 0, st>>>(in, n_images, h, w, out);
+  return check_launch("pyramid_down");
+}
+
+int launch_solve(const double* sums, int64_t count, double c_min, int level, double* est, int64_t stride,
+                 cudaStream_t st) {
+  if (count == 0) return CT_OK;
+  ttc_solve_kernel<<<(unsigned)cdiv(count, 128), 128, 0, st>>>(sums, count, c_min, level, est, stride);
+  return check_launch("ttc_solve");
+}
+
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// number of pyramid levels the reference visits for frames of h x w
+int ms_levels(int h, int w, int max_level) {
+  if (std::min(h, w) < 4) return 0;
+  int n = 1;
+  int lh = h, lw = w;
+  for (int l = 0; l < max_level; ++l) {
+    if (std::min(lh / 2, lw / 2) < 4) break;
+    lh /= 2;
+    lw /= 2;
+    ++n;
+  }
+  return n;
+}
+
+template <typename T>
+size_t run_seq_ws(int64_t nv, int nf, int h, int w, int level, int max_level) {
+  const bool ms = max_level >= 0;
+  const int nl = ms ? ms_levels(h, w, max_level) : level + 1;
+  size_t total = 0;
+  int lh = h, lw = w;
+  size_t mom = 0;
+  for (int l = 0; l < std::max(nl, 1); ++l) {
+    if (l > 0) total += align256((size_t)nv * nf * lh * lw * sizeof(T));
+    if (!ms && l != level) {
+      lh /= 2;
+      lw /= 2;
+      continue;
+    }
+    mom = std::max(mom, moments_ws_bytes<T>(nv, nf, lh, lw));
+    lh /= 2;
+    lw /= 2;
+  }
+  const int64_t np = nv * (nf - 1);
+  total += align256(mom);
+  total += align256((size_t)np * 11 * sizeof(double));
+  if (ms) total += align256((size_t)np * std::max(nl, 1) * 10 * sizeof(double));
+  return total;
+}
+
+template <typename T>
+int run_seq(const T* frames, int64_t nv, int nf, int h, int w, int level, int max_level, double c_min,
+            double* est, void* ws, size_t ws_bytes, cudaStream_t st) {
+  const bool ms = max_level >= 0;
+  const int64_t np = nv * (nf - 1);
+  if (np <= 0) return CT_OK;
+  const size_t need = run_seq_ws<T>(nv, nf, h, w, level, max_level);
+  CT_REQUIRE(ws != nullptr && ws_bytes >= need, "run_sequence workspace too small (%zu < %zu)", ws_bytes, need);
+  const int nl = ms ? ms_levels(h, w, max_level) : level + 1;
+  char* cur = reinterpret_cast<char*>(ws);
+  // pyramid levels 1..nl-1
+  const T* lv = frames;
+  int lh = h, lw = w;
+  const T* level_ptr[32];
+  int level_h[32], level_w[32];
+  level_ptr[0] = frames;
+  level_h[0] = h;
+  level_w[0] = w;
+  for (int l = 1; l < nl; ++l) {
+    T* dst = reinterpret_cast<T*>(cur);
+    cur += align256((size_t)nv * nf * (lh / 2) * (lw / 2) * sizeof(T));
+    int rc = launch_pyramid<T>(lv, nv * nf, lh, lw, dst, st);
+    if (rc) return rc;
+    lv = dst;
+    lh /= 2;
+    lw /= 2;
+    level_ptr[l] = dst;
+    level_h[l] = lh;
+    level_w[l] = lw;
+  }
+  size_t mom = 0;
+  for (int l = 0; l < nl; ++l)
+    if (ms || l == level) mom = std::max(mom, moments_ws_bytes<T>(nv, nf, level_h[l], level_w[l]));
+  void* mom_ws = cur;
+  cur += align256(mom);
+  double* sums = reinterpret_cast<double*>(cur);
+  cur += align256((size_t)np * 11 * sizeof(double));
+  if (!ms) {
+    int rc = launch_moments<T>(level_ptr[level], nv, nf, level_h[level], level_w[level], 1, sums, mom_ws, mom, st);
+    if (rc) return rc;
+    return launch_solve(sums, np, c_min, level, est, 10, st);
+  }
+  if (nl == 0) {
+    multiscale_select_kernel<<<(unsigned)cdiv(np, 128), 128, 0, st>>>(nullptr, np, 0, est);
+    return check_launch("multiscale_select");
+  }
+  double* est_levels = reinterpret_cast<double*>(cur);
+  for (int l = 0; l < nl; ++l) {
+    int rc = launch_moments<T>(level_ptr[l], nv, nf, level_h[l], level_w[l], 1, sums, mom_ws, mom, st);
+    if (rc) return rc;
+    rc = launch_solve(sums, np, c_min, l, est_levels + l * 10, (int64_t)nl * 10, st);
+    if (rc) return rc;
+  }
+  multiscale_select_kernel<<<(unsigned)cdiv(np, 128), 128, 0, st>>>(est_levels, np, nl, est);
+  return check_launch("multiscale_select");
+}
+
+}  // namespace
+}  // namespace ct
+
+using namespace ct;
+
+#define CT_DT_CHECK(dtype) CT_REQUIRE((dtype) == CT_F64 || (dtype) == CT_F32, "dtype must be CT_F64 or CT_F32")
+
+extern "C" int ct_ttc_derivatives(int dtype, const void* first, const void* second, int64_t h, int64_t w,
+                                  void* ex, void* ey, void* et, void* stream) {
+  clear_error();
+  CT_DT_CHECK(dtype);
+  CT_REQUIRE(h >= 2 && w >= 2, "need extents >= 2 for derivatives, got (%lld, %lld)", (long long)h, (long long)w);
+  CT_REQUIRE(h < (1 << 30) && w < (1 << 30), "extent too large");
+  const int64_t n = (h - 1) * (w - 1);
+  const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(n, 256), (int64_t)num_sms() * 16);
+  cudaStream_t st = as_stream(stream);
+  if (dtype == CT_F64)
+    deriv_fields_kernel<double><<<blocks, 256, 0, st>>>((const double*)first, (const double*)second, (int)h,
+                                                         (int)w, (double*)ex, (double*)ey, (double*)et);
+  else
+    deriv_fields_kernel<float><<<blocks, 256, 0, st>>>((const float*)first, (const float*)second, (int)h, (int)w,
+                                                        (float*)ex, (float*)ey, (float*)et);
+  return check_launch("derivatives");
+}
+
+extern "C" int ct_radial_gradient(int dtype, const void* ex, const void* ey, int64_t gh, int64_t gw, void* g,
+                                  void* stream) {
+  clear_error();
+  CT_DT_CHECK(dtype);
+  CT_REQUIRE(gh >= 0 && gw >= 0 && gh < (1 << 30) && gw < (1 << 30), "bad extents");
+  const int64_t n = gh * gw;
+  if (n == 0) return CT_OK;
+  const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(n, 256), (int64_t)num_sms() * 16);
+  cudaStream_t st = as_stream(stream);
+  if (dtype == CT_F64)
+    radial_gradient_kernel<double><<<blocks, 256, 0, st>>>((const double*)ex, (const double*)ey, (int)gh, (int)gw,
+                                                            (double*)g);
+  else
+    radial_gradient_kernel<float><<<blocks, 256, 0, st>>>((const float*)ex, (const float*)ey, (int)gh, (int)gw,
+                                                           (float*)g);
+  return check_launch("radial_gradient");
+}
+
+extern "C" size_t ct_normal_system_workspace_bytes(int64_t gh, int64_t gw) {
+  (void)gh;
+  (void)gw;
+  return (size_t)kNsBlocks * 10 * sizeof(double);
+}
+
+extern "C" int ct_normal_system(int dtype, const void* ex, const void* ey, const void* g, const void* et, int64_t gh,
+                                int64_t gw, int64_t border, double* sums, void* workspace, size_t workspace_bytes,
+                                void* stream) {
+  clear_error();
+  CT_DT_CHECK(dtype);
+  CT_REQUIRE(border >= 1, "border must cover the derivative-kernel radius (>= 1)");
+  CT_REQUIRE(gh > 2 * border && gw > 2 * border, "no interior left: grid (%lld, %lld), border %lld", (long long)gh,
+             (long long)gw, (long long)border);
+  CT_REQUIRE(workspace && workspace_bytes >= ct_normal_system_workspace_bytes(gh, gw), "workspace too small");
+  cudaStream_t st = as_stream(stream);
+  double* partials = reinterpret_cast<double*>(workspace);
+  if (dtype == CT_F64)
+    normal_system_kernel<double><<<kNsBlocks, kNsThreads, 0, st>>>((const double*)ex, (const double*)ey,
+                                                                    (const double*)g, (const double*)et, (int)gh,
+                                                                    (int)gw, (int)border, partials);
+  else
+    normal_system_kernel<float><<<kNsBlocks, kNsThreads, 0, st>>>((const float*)ex, (const float*)ey,
+                                                                   (const float*)g, (const float*)et, (int)gh,
+                                                                   (int)gw, (int)border, partials);
+  int rc = check_launch("normal_system");
+  if (rc) return rc;
+  const double count = (double)(gh - 2 * border) * (double)(gw - 2 * border);
+  moments_finalize_kernel<<<1, 32, 0, st>>>(partials, 1, kNsBlocks, count, sums);
+  return check_launch("normal_system_finalize");
+}
+
+extern "C" size_t ct_ttc_moments_workspace_bytes(int dtype, int64_t n_videos, int64_t n_frames, int64_t h,
+                                                 int64_t w) {
+  if (dtype == CT_F64) return moments_ws_bytes<double>(n_videos, (int)n_frames, (int)h, (int)w);
+  return moments_ws_bytes<float>(n_videos, (int)n_frames, (int)h, (int)w);
+}
+
+extern "C" int ct_ttc_moments(int dtype, const void* frames, int64_t n_videos, int64_t n_frames, int64_t h,
+                              int64_t w, double* sums, void* workspace, size_t workspace_bytes, void* stream) {
+  clear_error();
+  CT_DT_CHECK(dtype);
+  CT_REQUIRE(n_frames >= 2, "need at least two frames");
+  CT_REQUIRE(h >= 4 && w >= 4, "frames of (%lld, %lld) leave no interior, need >= 4", (long long)h, (long long)w);
+  CT_REQUIRE(h < (1 << 30) && w < (1 << 30) && n_frames < (1 << 30) && n_videos >= 0, "bad extents");
+  cudaStream_t st = as_stream(stream);
+  if (dtype == CT_F64)
+    return launch_moments<double>((const double*)frames, n_videos, (int)n_frames, (int)h, (int)w, 1, sums, workspace,
+                                  workspace_bytes, st);
+  return launch_moments<float>((const float*)frames, n_videos, (int)n_frames, (int)h, (int)w, 1, sums, workspace,
+                               workspace_bytes, st);
+}
+
+extern "C" int ct_ttc_solve(const double* sums, int64_t count, double c_min, int level, double* est, void* stream) {
+  clear_error();
+  CT_REQUIRE(count >= 0 && level >= 0, "bad arguments");
+  return launch_solve(sums, count, c_min, level, est, 10, as_stream(stream));
+}
+
+extern "C" int ct_pyramid_down(int dtype, const void* in, int64_t n_images, int64_t h, int64_t w, void* out,
+                               void* stream) {
+  clear_error();
+  CT_DT_CHECK(dtype);
+  CT_REQUIRE(h >= 2 && w >= 2, "cannot halve extents (%lld, %lld)", (long long)h, (long long)w);
+  CT_REQUIRE(h < (1 << 30) && w < (1 << 30) && n_images >= 0, "bad extents");
+  cudaStream_t st = as_stream(stream);
+  if (dtype == CT_F64) return launch_pyramid<double>((const double*)in, n_images, (int)h, (int)w, (double*)out, st);
+  return launch_pyramid<float>((const float*)in, n_images, (int)h, (int)w, (float*)out, st);
+}
+
+extern "C" int ct_ttc_multiscale_select(const double* est_levels, int64_t count, int n_levels, double* best,
+                                        void* stream) {
+  clear_error();
+  CT_REQUIRE(count >= 0 && n_levels >= 0, "bad arguments");
+  if (count == 0) return CT_OK;
+  multiscale_select_kernel<<<(unsigned)cdiv(count, 128), 128, 0, as_stream(stream)>>>(est_levels, count, n_levels,
+                                                                                      best);
+  return check_launch("multiscale_select");
+}
+
+extern "C" size_t ct_run_sequence_workspace_bytes(int dtype, int64_t n_videos, int64_t n_frames, int64_t h, int64_t w,
+                                                  int level, int max_level) {
+  if (n_frames < 2 || h < 1 || w < 1) return 0;
+  if (dtype == CT_F64) return run_seq_ws<double>(n_videos, (int)n_frames, (int)h, (int)w, level, max_level);
+  return run_seq_ws<float>(n_videos, (int)n_frames, (int)h, (int)w, level, max_level);
+}
+
+static int check_run_seq_args(int64_t n_frames, int64_t h, int64_t w, int level, int max_level) {
+  CT_REQUIRE(n_frames >= 2, "need at least two frames");
+  CT_REQUIRE(h < (1 << 30) && w < (1 << 30) && n_frames < (1 << 30), "extent too large");
+  if (max_level < 0) {
+    CT_REQUIRE(level >= 0, "level must be >= 0");
+    int64_t lh = h, lw = w;
+    for (int i = 0; i < level; ++i) {
+      lh /= 2;
+      lw /= 2;
+    }
+    CT_REQUIRE(lh >= 4 && lw >= 4, "extents (%lld, %lld) leave (%lld, %lld) after %d halvings, need >= 4",
+               (long long)h, (long long)w, (long long)lh, (long long)lw, level);
+  }
+  CT_REQUIRE(max_level < 31 && level < 31, "level too large");
+  return CT_OK;
+}
+
+extern "C" int ct_run_sequence(int dtype, const void* frames, int64_t n_videos, int64_t n_frames, int64_t h,
+                               int64_t w, int level, int max_level, double c_min, double* est, void* workspace,
+                               size_t workspace_bytes, void* stream) {
+  clear_error();
+  CT_DT_CHECK(dtype);
+  int rc = check_run_seq_args(n_frames, h, w, level, max_level);
+  if (rc) return rc;
+  cudaStream_t st = as_stream(stream);
+  if (dtype == CT_F64)
+    return run_seq<double>((const double*)frames, n_videos, (int)n_frames, (int)h, (int)w, level, max_level, c_min,
+                           est, workspace, workspace_bytes, st);
+  return run_seq<float>((const float*)frames, n_videos, (int)n_frames, (int)h, (int)w, level, max_level, c_min, est,
+                        workspace, workspace_bytes, st);
+}

@@ -1,0 +1,156 @@
+"""Synthetic approach sequences generated on the device (inputs for tests and the benchmark).
+
+Mirrors convtact.synth (/root/reference/pkg/src/convtact/synth.py):
+  * make_texture: PCG64(seed) uniform noise (drawn on the host with numpy's
+    generator, the same stream as the reference), two 3x3 binomial SAME /
+    REPLICATE passes through this package's conv engine on the device, then
+    a min-max rescale (synth.py:68-85);
+  * zoom frames: separable Catmull-Rom magnification about the FOE, done by
+    ct_zoom_frames (synth.py:88-126), bit-identical in float64;
+  * generate(SynthConfig): frames t = 0..frames-1 with magnification
+    t0 / (t0 - t) (synth.py:129-143); sensor noise from the independent
+    PCG64(SeedSequence([seed, 1])) stream when noise_sigma > 0.
+
+approach_stream() implements the long-video rule used for BASELINE config 5
+(SURVEY.md D3): the reference forbids frames >= t0, so a 1024-frame stream is
+a sequence of approach segments, each with its own seeded texture and
+T0 ~ U[50, 500], cut while the true time to contact is still >= 20 frames.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .conv import BoundaryPolicy, ConvShape, direct_batch
+
+_B3 = np.outer(*(2 * [np.array([1.0, 2.0, 1.0]) / 4.0]))
+
+
+@dataclass(frozen=True)
+class SynthConfig:
+    width: int = 256
+    height: int = 256
+    frames: int = 60
+    t0: float = 100.0
+    foe: tuple[float, float] = (0.4, 0.55)
+    seed: int = 1
+    noise_sigma: float = 0.0
+
+    def __post_init__(self):  # synth.py:40-55
+        if self.width < 16 or self.height < 16:
+            raise ValueError(f"size {self.width}x{self.height} too small, need >= 16")
+        if self.frames < 2:
+            raise ValueError("need at least 2 frames")
+        if not self.t0 > 0:
+            raise ValueError("t0 must be positive")
+        if self.frames >= self.t0:
+            raise ValueError(f"frames ({self.frames}) must stay short of contact at t0 ({self.t0})")
+        fx, fy = self.foe
+        if not (0.0 < fx < 1.0 and 0.0 < fy < 1.0):
+            raise ValueError(f"foe fractions must lie inside (0, 1), got {self.foe}")
+        if self.noise_sigma < 0:
+            raise ValueError("noise_sigma must be >= 0")
+
+    @property
+    def foe_px(self) -> tuple[float, float]:
+        return self.foe[0] * self.width, self.foe[1] * self.height
+
+
+def make_texture(width: int, height: int, seed: int, device="cuda") -> torch.Tensor:
+    """Band-limited random texture in [0, 1] as a float64 CUDA tensor (synth.py:68-85)."""
+    if width < 16 or height < 16:
+        raise ValueError(f"texture {width}x{height} too small, need >= 16")
+    rng = np.random.Generator(np.random.PCG64(seed))
+    img = torch.from_numpy(rng.random((height, width))).to(device)
+    for _ in range(2):
+        img = direct_batch(img[None], _B3, ConvShape.SAME, BoundaryPolicy.REPLICATE, flip=False)[0]
+    lo, hi = img.min(), img.max()
+    if not bool(hi > lo):
+        return torch.zeros_like(img)
+    return (img - lo) / (hi - lo)
+
+
+def zoom_frames(texture: torch.Tensor, foe_px, mags, dtype=torch.float64, out: torch.Tensor | None = None):
+    """frames[t] = zoom_frame(texture, foe_px, mags[t]) on the device -> [len(mags), h, w]."""
+    tex = texture.contiguous()
+    if tex.dtype != torch.float64 or not tex.is_cuda:
+        raise TypeError("texture must be a float64 CUDA tensor")
+    h, w = tex.shape
+    m = np.ascontiguousarray(mags, dtype=np.float64)
+    if out is None:
+        out = torch.empty((len(m), h, w), dtype=dtype, device=tex.device)
+    L = _lib.load()
+    _lib.check(L.ct_zoom_frames(_lib.dtype_code(out), _lib.ptr(tex), h, w, float(foe_px[0]), float(foe_px[1]),
+                                m.ctypes.data_as(ctypes.c_void_p), len(m), _lib.ptr(out), None, 0,
+                                _lib.stream_ptr()))
+    return out
+
+
+def generate(cfg: SynthConfig, dtype=torch.float64) -> tuple[torch.Tensor, np.ndarray]:
+    """(frames [frames, h, w] on the device, truth rows (frame, ttc, foe_x, foe_y)) (synth.py:129-143)."""
+    tex = make_texture(cfg.width, cfg.height, cfg.seed)
+    mags = [cfg.t0 / (cfg.t0 - t) for t in range(cfg.frames)]
+    frames = zoom_frames(tex, cfg.foe_px, mags, dtype=torch.float64)
+    if cfg.noise_sigma > 0:
+        noise_rng = np.random.Generator(np.random.PCG64(np.random.SeedSequence([cfg.seed, 1])))
+        for t in range(cfg.frames):
+            noise = torch.from_numpy(noise_rng.normal(0.0, cfg.noise_sigma, (cfg.height, cfg.width))).to(frames.device)
+            frames[t] = torch.clamp(frames[t] + noise, 0.0, 1.0)
+    fx, fy = cfg.foe_px
+    truth = np.array([(t, cfg.t0 - t, fx, fy) for t in range(cfg.frames)], dtype=np.float64)
+    return frames.to(dtype), truth
+
+
+@dataclass(frozen=True)
+class Segment:
+    start: int
+    length: int
+    t0: float
+    texture_seed: int
+
+
+def approach_segments(frames: int, seed: int, t0_range=(50.0, 500.0), min_ttc: float = 20.0) -> list[Segment]:
+    """Split a long stream into approach segments.
+
+    Segment k draws T0_k ~ U[t0_range] and a texture seed from PCG64(seed);
+    it lasts floor(T0_k - min_ttc) + 1 frames (true TTC >= min_ttc on every
+    frame) or until the stream ends.  The pair spanning a cut has no truth.
+    """
+    rng = np.random.Generator(np.random.PCG64(seed))
+    segs, start = [], 0
+    while start < frames:
+        t0 = float(rng.uniform(*t0_range))
+        tex_seed = int(rng.integers(0, 2**31 - 1))
+        length = min(frames - start, int(math.floor(t0 - min_ttc)) + 1)
+        segs.append(Segment(start, length, t0, tex_seed))
+        start += length
+    return segs
+
+
+def approach_stream(frames: int, height: int, width: int, seed: int, dtype=torch.float32,
+                    out: torch.Tensor | None = None, foe=(0.5, 0.5)) -> tuple[torch.Tensor, np.ndarray]:
+    """A long synthetic approach video on the device (BASELINE config 5 inputs).
+
+    Returns (frames [frames, h, w] in ``dtype``, truth ttc per frame with NaN
+    on the first frame of every segment after the first -- the pair ending
+    there spans a cut).  Frames are generated in float64 and rounded to
+    ``dtype`` (SURVEY.md section 8(d) seeding convention).
+    """
+    if out is None:
+        out = torch.empty((frames, height, width), dtype=dtype, device="cuda")
+    truth = np.empty(frames)
+    foe_px = (foe[0] * width, foe[1] * height)
+    for s in approach_segments(frames, seed):
+        tex = make_texture(width, height, s.texture_seed)
+        mags = [s.t0 / (s.t0 - t) for t in range(s.length)]
+        zoom_frames(tex, foe_px, mags, dtype=dtype, out=out[s.start:s.start + s.length])
+        truth[s.start:s.start + s.length] = [s.t0 - t for t in range(s.length)]
+        if s.start > 0:
+            truth[s.start] = np.nan
+    return out, truth

@@ -1,0 +1,237 @@
+"""GPU parity of the TTC path (K5-K7 + pyramid + generator) against the
+reference fixtures and the CPU oracle.
+
+Tolerances (BASELINE north_star, relative inf-norm per SURVEY.md D5):
+  * float64 derivative fields, G, downsample, generator frames: bit-exact
+    (same per-element operation order as the reference);
+  * float64 normal-system sums: 1e-12 relative (reduction order differs);
+  * float64 per-pair TTC (and a, b, c, FOE): 1e-9 relative;
+  * float32 path (config 5 convention, oracle = float64 reference on the
+    float32-rounded frames): sums and TTC within 1e-4 relative.
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import paper_1612_08825_b200 as ct
+from conftest import rel_inf
+from paper_1612_08825_b200 import FramePair, NormalSystem
+
+pytestmark = pytest.mark.gpu
+
+EST = ("a", "b", "c", "x0", "y0", "ttc", "residual", "misfit", "level", "degenerate")
+
+
+def rows(ests):
+    return np.array([[float(getattr(e, f)) for f in EST] for e in ests])
+
+
+def assert_est_close(got, ref, rtol, fields=(0, 1, 2, 3, 4, 5)):
+    got = np.asarray(got)
+    ref = np.asarray(ref)
+    assert got.shape == ref.shape
+    assert np.array_equal(got[..., 8], ref[..., 8]), "level differs"
+    assert np.array_equal(got[..., 9], ref[..., 9]), "degenerate flag differs"
+    for f in fields:
+        g, r = got[..., f], ref[..., f]
+        assert np.array_equal(np.isnan(g), np.isnan(r)), EST[f]
+        fin = np.isfinite(r)
+        assert np.array_equal(np.isinf(g), np.isinf(r)), EST[f]
+        if fin.any():
+            err = np.max(np.abs(g[fin] - r[fin]) / np.maximum(np.abs(r[fin]), 1e-300))
+            assert err <= rtol, f"{EST[f]} rel err {err:.3e} > {rtol}"
+
+
+@pytest.fixture(scope="module")
+def cfg2_frames():
+    return O.generate(256, 256, 64, 100.0, (0.5, 0.5), 0, 0.0)
+
+
+def test_device_generator_bit_exact(golden, cfg2_frames):
+    t = golden("ttc_fixtures.npz")
+    frames, truth = ct.generate(ct.SynthConfig(width=256, height=256, frames=64, t0=100.0, foe=(0.5, 0.5), seed=0))
+    f = frames.cpu().numpy()
+    assert hashlib.sha256(f.tobytes()).hexdigest() == str(t["cfg2_frames_sha"])
+    assert np.array_equal(truth[:, 1], 100.0 - np.arange(64))
+    fn, _ = ct.generate(ct.SynthConfig(width=128, height=128, frames=12, t0=60.0, foe=(0.5, 0.5), seed=2,
+                                       noise_sigma=0.05))
+    assert hashlib.sha256(fn.cpu().numpy().tobytes()).hexdigest() == str(t["noisy_frames_sha"])
+
+
+def test_fields_bit_exact(golden):
+    t = golden("ttc_fixtures.npz")
+    a, b = t["small_a"], t["small_b"]
+    ex, ey, et = ct.derivatives_3d(FramePair(a, b))
+    assert np.array_equal(ex, t["small_ex"]) and np.array_equal(ey, t["small_ey"]) and np.array_equal(et, t["small_et"])
+    g = ct.radial_gradient(ex, ey)
+    assert np.array_equal(g, t["small_g"])
+    ns = ct.build_normal_system(ex, ey, g, et, border=1)
+    ref = t["small_sums_b1"]
+    got = np.array([ns.m[0, 0], ns.m[0, 1], ns.m[0, 2], ns.m[1, 1], ns.m[1, 2], ns.m[2, 2], *ns.rhs, ns.et2, ns.count])
+    assert np.max(np.abs(got - ref) / np.abs(ref)) <= 1e-12
+    ns3 = ct.build_normal_system(ex, ey, g, et, border=3)
+    assert ns3.count == t["small_sums_b3"][10]
+    assert np.array_equal(ct.downsample(a), t["small_down"])
+    assert np.array_equal(ct.downsample(ct.downsample(a)), t["small_down2"])
+
+
+def test_solver_bit_exact_given_sums(golden):
+    t = golden("ttc_fixtures.npz")
+    s = t["small_sums_b1"]
+    sys_ = NormalSystem(m=np.array([[s[0], s[1], s[2]], [s[1], s[3], s[4]], [s[2], s[4], s[5]]]), rhs=s[6:9],
+                        et2=s[9], count=int(s[10]))
+    est = ct.solve_ttc(sys_)
+    assert np.array_equal(rows([est])[0], t["small_est"], equal_nan=True)
+
+
+def test_solver_reference_cases():  # test_ttc.py:80-122
+    rng = np.random.default_rng(42)
+    for _ in range(50):
+        r = rng.standard_normal((3, 3))
+        m = r.T @ r + 1e-3 * np.eye(3)
+        rhs = rng.standard_normal(3)
+        est = ct.solve_ttc(NormalSystem(m=m, rhs=rhs, et2=50.0, count=10))
+        assert not est.degenerate
+        assert np.allclose([est.a, est.b, est.c], np.linalg.solve(m, rhs), rtol=1e-8, atol=1e-10)
+        sums = np.array([m[0, 0], m[0, 1], m[0, 2], m[1, 1], m[1, 2], m[2, 2], *rhs, 50.0, 10.0])
+        assert np.array_equal(rows([est])[0], O.solve_ttc(sums), equal_nan=True)
+    est = ct.solve_ttc(NormalSystem(m=np.diag([2.0, 4.0, 8.0]), rhs=np.array([2.0, 4.0, 8.0]), et2=20.0, count=4))
+    assert est.residual == pytest.approx(1.5) and est.misfit == pytest.approx(0.3)
+    assert est.ttc == pytest.approx(1.0) and est.x0 == pytest.approx(-1.0) and est.y0 == pytest.approx(-1.0)
+    zero = ct.solve_ttc(NormalSystem(m=np.zeros((3, 3)), rhs=np.zeros(3), et2=0.0, count=9))
+    assert zero.degenerate and np.isnan(zero.ttc) and np.isinf(zero.misfit)
+    assert ct.solve_ttc(NormalSystem(m=np.diag([1.0, 1.0, 1e-15]), rhs=np.ones(3), et2=1.0, count=9)).degenerate
+    inf = ct.solve_ttc(NormalSystem(m=np.eye(3), rhs=np.array([0.5, -0.25, 0.0]), et2=1.0, count=4))
+    assert not inf.degenerate and np.isinf(inf.ttc) and inf.ttc > 0 and np.isnan(inf.x0) and inf.a == pytest.approx(0.5)
+
+
+def test_cfg2_run_sequence_level0(golden, cfg2_frames):
+    t = golden("ttc_fixtures.npz")
+    got = rows(ct.run_sequence(cfg2_frames, level=0))
+    assert_est_close(got, t["cfg2_l0"], 1e-9, fields=(0, 1, 2, 3, 4, 5, 6, 7))
+    # SURVEY.md 8(c) anchors
+    assert got[0, 5] == pytest.approx(97.315722253398093, rel=1e-9)
+    assert got[31, 5] == pytest.approx(63.514498981613194, rel=1e-9)
+    assert got[62, 5] == pytest.approx(33.849933824360562, rel=1e-9)
+
+
+@pytest.mark.parametrize("key,kw", [("cfg2_l1", dict(level=1)), ("cfg2_l2", dict(level=2)),
+                                    ("cfg2_ms5", dict(max_level=5))])
+def test_cfg2_levels_and_multiscale(golden, cfg2_frames, key, kw):
+    t = golden("ttc_fixtures.npz")
+    got = rows(ct.run_sequence(cfg2_frames[:9], **kw))
+    assert_est_close(got, t[key], 1e-9)
+
+
+def test_device_resident_batch_matches_host_path(cfg2_frames):
+    f = torch.from_numpy(cfg2_frames).cuda()
+    batch = torch.stack([f, f.flip(0), f * 0.5 + 0.25])
+    est = ct.run_sequence_batch(batch, level=0).cpu().numpy()
+    for v in range(3):
+        ref = O.run_sequence(batch[v].cpu().numpy(), level=0)
+        assert_est_close(est[v], ref, 1e-9, fields=(0, 1, 2, 3, 4, 5, 6, 7))
+    host = ct.run_sequence_host(batch.cpu().numpy(), level=0)
+    assert np.array_equal(host, est)  # same kernels, same reduction order -> identical
+
+
+def test_moments_sums_vs_oracle_fp64(cfg2_frames):
+    from paper_1612_08825_b200 import _lib
+    f = torch.from_numpy(cfg2_frames[:12]).cuda()
+    L = _lib.load()
+    n = 12
+    sums = torch.empty((n - 1, 11), dtype=torch.float64, device="cuda")
+    nb = L.ct_ttc_moments_workspace_bytes(_lib.CT_F64, 1, n, 256, 256)
+    ws = _lib.workspace(nb, "cuda")
+    _lib.check(L.ct_ttc_moments(_lib.CT_F64, _lib.ptr(f), 1, n, 256, 256, _lib.ptr(sums), _lib.ptr(ws), nb,
+                                _lib.stream_ptr()))
+    got = sums.cpu().numpy()
+    for i in range(n - 1):
+        ex, ey, et = O.derivatives(cfg2_frames[i], cfg2_frames[i + 1])
+        ref = O.normal_system(ex, ey, O.radial_gradient(ex, ey), et, 1)
+        assert np.max(np.abs(got[i] - ref) / np.abs(ref)) <= 1e-12, i
+
+
+def test_odd_shapes_fallback_loader():
+    # widths whose rows are not 16-byte multiples take the non-TMA loader
+    rng = np.random.default_rng(3)
+    for h, w in [(37, 50), (33, 257), (300, 29), (5, 5), (64, 511)]:
+        fr = O.generate(max(w, 16), max(h, 16), 4, 30.0, (0.4, 0.6), 7, 0.0)[:, :h, :w] + 0.01 * rng.random((4, h, w))
+        got = rows(ct.run_sequence(fr, level=0))
+        assert_est_close(got, O.run_sequence(fr, level=0), 1e-9, fields=(0, 1, 2, 3, 4, 5, 6, 7))
+
+
+def test_noisy_multiscale_vs_reference(golden):
+    t = golden("ttc_fixtures.npz")
+    fn, _ = ct.generate(ct.SynthConfig(width=128, height=128, frames=12, t0=60.0, foe=(0.5, 0.5), seed=2,
+                                       noise_sigma=0.05))
+    got = rows(ct.run_sequence(fn.cpu().numpy(), max_level=5))
+    assert_est_close(got, t["noisy_ms5"], 1e-9)
+    got0 = rows(ct.run_sequence(fn, level=0))  # device tensor input
+    assert_est_close(got0, t["noisy_l0"], 1e-9)
+
+
+def test_fp32_multiscale_config5_convention(golden):
+    t = golden("ttc_fixtures.npz")
+    f64 = O.generate(480, 270, 4, 300.0, (0.5, 0.5), 11, 0.0)
+    f32 = torch.from_numpy(f64.astype(np.float32)).cuda()
+    est = ct.run_sequence_batch(f32[None], max_level=3).cpu().numpy()[0]
+    ref = t["c5_ms3"]
+    assert np.array_equal(est[:, 8], ref[:, 8])
+    assert_est_close(est, ref, 1e-4, fields=(2, 5))
+    # each level separately
+    for lv in range(4):
+        e = ct.run_sequence_batch(f32[None, :2], level=lv).cpu().numpy()[0, 0]
+        assert abs(e[5] - t["c5_l"][lv][5]) <= 1e-4 * abs(t["c5_l"][lv][5]), lv
+    # fp32 pyramid level vs float64 reference downsample of the rounded frame
+    d = ct.downsample(f32[0]).cpu().numpy()
+    assert rel_inf(d, t["c5_down"]) <= 1e-6
+
+
+def test_degenerate_and_none_semantics():  # test_ttc.py:125-129, 200-212
+    est = ct.estimate_fixed(FramePair(np.full((32, 32), 0.5), np.full((32, 32), 0.5)), level=0)
+    assert est.degenerate and np.isnan(est.ttc)
+    assert ct.estimate_multiscale(FramePair(np.zeros((32, 32)), np.zeros((32, 32))), max_level=3).degenerate
+    assert ct.estimate_multiscale(FramePair(np.ones((3, 8)), np.ones((3, 8))), max_level=2) is None
+    with pytest.raises(ValueError):
+        ct.estimate_fixed(FramePair(np.ones((16, 16)), np.ones((16, 16))), level=3)
+    with pytest.raises(ValueError):
+        ct.estimate_fixed(FramePair(np.ones((16, 16)), np.ones((16, 16))), level=-1)
+    with pytest.raises(ValueError):
+        ct.run_sequence(np.ones((1, 8, 8)))
+    with pytest.raises(ValueError):
+        ct.run_sequence(np.ones((8, 8)))
+    with pytest.raises(ValueError):
+        FramePair(np.ones((3, 3)), np.ones((3, 4)))
+
+
+def test_multiscale_zero_levels_equals_fixed():  # test_ttc.py:190-197
+    f = O.generate(64, 64, 2, 30.0, (0.5, 0.5), 6, 0.0)
+    pair = FramePair(f[0], f[1])
+    ms = ct.estimate_multiscale(pair, max_level=0)
+    fx = ct.estimate_fixed(pair, level=0)
+    assert ms.level == 0 and ms.ttc == fx.ttc
+
+
+def test_shard_count_invariance_bitwise(cfg2_frames):
+    # temporal sharding with a one-frame halo gives identical rows (no cross-pair state)
+    full = ct.run_sequence_batch(torch.from_numpy(cfg2_frames).cuda()[None], level=0)[0].cpu().numpy()
+    for shards in (2, 3, 8):
+        bounds = np.linspace(0, 63, shards + 1).astype(int)
+        parts = [ct.run_sequence_batch(torch.from_numpy(cfg2_frames[a:b + 1]).cuda()[None], level=0)[0].cpu().numpy()
+                 for a, b in zip(bounds[:-1], bounds[1:])]
+        assert np.array_equal(np.concatenate(parts), full)
+
+
+def test_full_size_batch_properties():
+    # size-independent checks at the bench size: pair (t, t) gives Et == 0 -> zero
+    # misfit numerator and degenerate-free; swapping every frame pair in time flips c
+    f, _ = ct.generate(ct.SynthConfig(width=256, height=256, frames=64, t0=100.0, foe=(0.5, 0.5), seed=0))
+    fwd = ct.run_sequence_batch(f[None], level=0)[0].cpu().numpy()
+    rev = ct.run_sequence_batch(f.flip(0)[None], level=0)[0].cpu().numpy()[::-1]
+    # reversing time negates Et: c (and a, b) flip sign exactly
+    assert np.array_equal(rev[:, 2], -fwd[:, 2])
+    assert np.array_equal(rev[:, 0], -fwd[:, 0])
