@@ -23,6 +23,7 @@
 // second kernel adds the partials in a fixed order, so results do not depend
 // on scheduling (bit-reproducible run to run and across shard counts).
 #include <math.h>
+#include <stdlib.h>
 
 #include <algorithm>
 
@@ -44,7 +45,11 @@ struct AccT<float> {
 };
 
 constexpr int kBoxCols = 256;     // frame columns per tile (TMA box inner extent)
-constexpr int kTileGridCols = 255;  // grid columns produced per tile
+constexpr int kTileGridCols = 255;  // grid columns of a single-tile frame (w <= 256)
+// With several column tiles the tile stride is 252 grid columns: tile starts
+// must be 16-byte aligned for the TMA box (multiple of 4 f32 / 2 f64
+// elements); a box start at element 255 raises an illegal-instruction fault.
+constexpr int kTileStrideMulti = 252;
 constexpr int kMomThreads = 128;  // 2 grid columns per thread
 
 struct MomentArgs {
@@ -57,6 +62,7 @@ struct MomentArgs {
   int n_bands, n_ctiles, units;
   int chunk;  // pairs per CTA
   int use_tma;
+  int tile_cols;  // grid columns per tile (255 single tile, 252 otherwise)
 };
 
 template <typename T>
@@ -93,7 +99,7 @@ __global__ void __launch_bounds__(kMomThreads) ttc_moments_kernel(const MomentAr
   const int unit = blockIdx.x;
   const int band = unit / a.n_ctiles, ctile = unit - band * a.n_ctiles;
   const int gy0 = band * BR;                 // first grid row (== first frame row) of the band
-  const int cx0 = ctile * kTileGridCols;      // first grid column (== first frame column)
+  const int cx0 = ctile * a.tile_cols;        // first grid column (== first frame column)
   const int64_t v = blockIdx.z;
   const int n_pairs = a.n_frames - 1;
   const int p0 = blockIdx.y * a.chunk;
@@ -105,8 +111,8 @@ __global__ void __launch_bounds__(kMomThreads) ttc_moments_kernel(const MomentAr
   // this thread's two grid columns (local 2*tid, 2*tid+1)
   const int lc = 2 * tid;
   const int gxa = cx0 + lc, gxb = gxa + 1;
-  const bool ina = lc < kTileGridCols && gxa >= a.border && gxa < a.gw - a.border;
-  const bool inb = lc + 1 < kTileGridCols && gxb >= a.border && gxb < a.gw - a.border;
+  const bool ina = lc < a.tile_cols && gxa >= a.border && gxa < a.gw - a.border;
+  const bool inb = lc + 1 < a.tile_cols && gxb >= a.border && gxb < a.gw - a.border;
   const ACC xa = (ACC)((double)gxa - (double)(a.gw - 1) / 2.0);
   const ACC xb = (ACC)((double)gxb - (double)(a.gw - 1) / 2.0);
   const double ycen = (double)(a.gh - 1) / 2.0;
@@ -550,6 +556,8 @@ __global__ void __launch_bounds__(256) pyramid_down_kernel(const T* __restrict__
 
 template <typename T>
 int band_rows_for() {
+  static const int env_rows = getenv("CT_BAND_ROWS") ? atoi(getenv("CT_BAND_ROWS")) : 0;  // tuning switch
+  if (env_rows > 0) return env_rows;
   return sizeof(T) == 8 ? 16 : 32;
 }
 
@@ -559,7 +567,7 @@ size_t moments_smem_bytes(int br) {
 }
 
 struct MomentPlan {
-  int band_rows, n_bands, n_ctiles, units, chunk, n_chunks;
+  int band_rows, n_bands, n_ctiles, units, chunk, n_chunks, tile_cols;
 };
 
 template <typename T>
@@ -568,7 +576,8 @@ MomentPlan plan_moments(int64_t n_videos, int n_frames, int h, int w) {
   p.band_rows = band_rows_for<T>();
   const int gh = h - 1, gw = w - 1;
   p.n_bands = (gh + p.band_rows - 1) / p.band_rows;
-  p.n_ctiles = (gw + kTileGridCols - 1) / kTileGridCols;
+  p.tile_cols = gw <= kTileGridCols ? kTileGridCols : kTileStrideMulti;
+  p.n_ctiles = (gw + p.tile_cols - 1) / p.tile_cols;
   p.units = p.n_bands * p.n_ctiles;
   const int n_pairs = n_frames - 1;
   // enough CTAs for ~4 waves at 2 CTAs/SM, but at least 8 pairs per CTA so
@@ -613,9 +622,11 @@ int launch_moments(const T* frames, int64_t n_videos, int n_frames, int h, int w
   a.n_ctiles = p.n_ctiles;
   a.units = p.units;
   a.chunk = p.chunk;
+  a.tile_cols = p.tile_cols;
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof(tmap));
-  a.use_tma = encode_tmap_2d(&tmap, frames, sizeof(T), (uint64_t)w, (uint64_t)(n_videos * n_frames * (int64_t)h),
+  static const bool no_tma = getenv("CT_NO_TMA") != nullptr;  // debugging switch
+  a.use_tma = !no_tma && encode_tmap_2d(&tmap, frames, sizeof(T), (uint64_t)w, (uint64_t)(n_videos * n_frames * (int64_t)h),
                              kBoxCols, p.band_rows + 1)
                   ? 1
                   : 0;
