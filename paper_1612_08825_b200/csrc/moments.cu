@@ -1,0 +1,361 @@
+// K5: fused derivative stencils + radial gradient + normal-system moments
+// over every consecutive frame pair (replaces derivatives_3d +
+// radial_gradient + build_normal_system, ttc.py:82-120, inside the
+// run_sequence loop ttc.py:299-304).
+//
+// Layout and schedule
+//   * A CTA (256 threads, one grid column each) owns a band of BR grid rows x
+//     up to 255 grid columns of one video and walks a chunk of consecutive
+//     frames.  Frame bands (BR+1 rows x 256 columns) arrive by TMA into a
+//     3-deep ring of shared-memory buffers tracked by mbarriers: while pair
+//     (t-1, t) is computed from two resident buffers, frame t+1 is in flight.
+//     Every frame is read from HBM once per band (the one-row band halo is
+//     shared with the neighbouring CTA through L2); no derivative field is
+//     ever written.
+//   * Per pixel (4x-scaled stencils, the x0.25 of ttc.py:29-31 is applied as
+//     an exact x1/16 on the sums): P = a + b, D = b - a per frame column;
+//     hP = P[x] + P[x+1], dP = P[x+1] - P[x], sD = D[x] + D[x+1] per row;
+//     Ex' = dP_y + dP_y+1, Ey' = hP_y+1 - hP_y, Et' = sD_y + sD_y+1.
+//   * G = xc*Ex + yc*Ey is folded out algebraically: with H = yc*Ey a thread
+//     (fixed column, fixed xc) accumulates S = {Ex^2, ExEy, Ey^2, ExEt, EyEt,
+//     Et^2} and U = {Ex H, Ey H, H Et, H H}; then sum(Ex G) = xc S1 + U1,
+//     sum(Ey G) = xc S2 + U2, sum(G Et) = xc S4 + U3, sum(G^2) = xc^2 S1 +
+//     2 xc U1 + U4.  ~21 FP64 ops per grid pixel.
+//   * Per pair the 256 per-thread sums are reduced through shared memory in
+//     a fixed tree (the dead previous-frame buffer is the scratch), giving one
+//     partial per band; moments_finalize adds the band partials in a fixed
+//     order.  Results are bit-reproducible and independent of how pairs are
+//     chunked or sharded.
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "moments.cuh"
+#include "tma.cuh"
+
+namespace ct {
+namespace {
+
+constexpr int kBoxCols = 256;        // frame columns per tile (TMA box inner extent)
+constexpr int kTileGridCols = 255;   // grid columns when the frame fits one tile (w <= 256)
+// With several column tiles the stride is 252 grid columns: a TMA box must
+// start 16-byte aligned (a start at element 255 faults with an illegal
+// instruction), and 252 is a multiple of 4 f32 / 2 f64 elements.
+constexpr int kTileStrideMulti = 252;
+constexpr int kThreads = 256;        // one grid column per thread
+constexpr int kRedSeg = 16;          // reduction tree: 16 segments of 16 threads
+
+template <typename T>
+struct AccT {
+  using type = T;  // per-thread accumulation type (f64 frames: f64; f32 frames: f32)
+};
+
+struct MomentArgs {
+  const void* frames;
+  double* partials;  // [n_videos][n_pairs][units][10]
+  int64_t n_videos;
+  int n_frames;
+  int h, w, gh, gw, border;
+  int n_ctiles, units;
+  int chunk;      // pairs per CTA
+  int use_tma;
+  int tile_cols;  // grid columns per tile
+};
+
+template <typename T, int BR>
+struct Smem {
+  static constexpr size_t buf_elems = (size_t)(BR + 1) * kBoxCols + 8;  // +8: masked right-neighbour reads
+  static constexpr size_t buf_bytes = (buf_elems * sizeof(T) + 127) & ~size_t(127);
+  // f64 bands are large enough to host the reduction scratch in the dead
+  // buffer; f32 bands get a dedicated scratch
+  static constexpr bool red_in_buf = buf_bytes >= 10 * kThreads * sizeof(double);
+  static constexpr size_t red_bytes = red_in_buf ? 0 : 10 * kThreads * sizeof(double);
+  static constexpr size_t bars_off = 3 * buf_bytes + red_bytes;
+  static constexpr size_t part_off = bars_off + 64;
+  static constexpr size_t total = part_off + 10 * kRedSeg * sizeof(double);
+};
+
+template <typename T, int BR>
+__global__ void __launch_bounds__(kThreads, 2) ttc_moments_kernel(const MomentArgs a,
+                                                                  const __grid_constant__ CUtensorMap tmap) {
+  using ACC = typename AccT<T>::type;
+  using S = Smem<T, BR>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  auto buf = [&](int k) { return reinterpret_cast<T*>(smem + (size_t)k * S::buf_bytes); };
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::bars_off);
+  double* part = reinterpret_cast<double*>(smem + S::part_off);
+
+  const int tid = threadIdx.x;
+  const int unit = blockIdx.x;
+  const int band = unit / a.n_ctiles, ctile = unit - band * a.n_ctiles;
+  const int gy0 = band * BR;              // first grid row == first frame row of the band
+  const int cx0 = ctile * a.tile_cols;     // first grid column == first frame column
+  const int64_t v = blockIdx.z;
+  const int n_pairs = a.n_frames - 1;
+  const int p0 = blockIdx.y * a.chunk;
+  const int p1 = min(p0 + a.chunk, n_pairs);  // pairs [p0, p1) -> frames p0..p1
+  if (p0 >= p1) return;
+  const int nload = p1 - p0 + 1;
+  constexpr uint32_t kBoxBytes = (uint32_t)((BR + 1) * kBoxCols * sizeof(T));
+
+  const int gx = cx0 + tid;
+  const bool in_col = tid < a.tile_cols && gx >= a.border && gx < a.gw - a.border;
+  const double xc = (double)gx - (double)(a.gw - 1) / 2.0;
+  const ACC yc0 = (ACC)((double)gy0 - (double)(a.gh - 1) / 2.0);  // centred y of grid row gy0
+  const int64_t row0 = (v * a.n_frames) * (int64_t)a.h + gy0;     // band row of frame p: row0 + p*h
+  // band-local frame-row range r in [r_beg, r_end] whose grid row gy0 + r - 1 is interior
+  const int r_end = min(BR, a.gh - a.border - gy0);
+  const int r_beg = max(1, a.border - gy0 + 1);
+
+  auto issue = [&](int f) {  // frame p0+f -> buffer f%3
+    T* dst = buf(f % 3);
+    const int64_t grow = row0 + (int64_t)(p0 + f) * a.h;
+    if (a.use_tma) {
+      if (tid == 0) {
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&bars[f % 3], kBoxBytes);
+        tma_load_2d(dst, &tmap, &bars[f % 3], cx0, (int)grow);
+      }
+    } else {
+      const T* src = reinterpret_cast<const T*>(a.frames) + grow * a.w;
+      const int64_t rows_left = a.n_videos * a.n_frames * (int64_t)a.h - grow;
+      for (int idx = tid; idx < (BR + 1) * kBoxCols; idx += kThreads) {
+        const int r = idx / kBoxCols, c = idx - r * kBoxCols;
+        T val = T(0);
+        if (r < rows_left && cx0 + c < a.w) val = src[(int64_t)r * a.w + cx0 + c];
+        dst[idx] = val;
+      }
+    }
+  };
+
+  if (a.use_tma) {
+    if (tid == 0) {
+      for (int i = 0; i < 3; ++i) mbar_init(&bars[i], 1);
+      mbar_fence_init();
+    }
+    __syncthreads();
+    for (int f = 0; f < min(3, nload); ++f) issue(f);
+  } else {
+    issue(0);
+    issue(1);
+    __syncthreads();
+  }
+
+  for (int i = 0; i < p1 - p0; ++i) {
+    const int p = p0 + i;
+    if (a.use_tma) {
+      mbar_wait(&bars[i % 3], (uint32_t)((i / 3) & 1));
+      mbar_wait(&bars[(i + 1) % 3], (uint32_t)(((i + 1) / 3) & 1));
+    }
+    const T* A = buf(i % 3);
+    const T* B = buf((i + 1) % 3);
+
+    ACC s1 = 0, s2 = 0, s3 = 0, s4 = 0, s5 = 0, s6 = 0, u1 = 0, u2 = 0, u3 = 0, u4 = 0;
+    ACC hP, dP, sD;
+    {
+      const ACC a0 = (ACC)A[tid], a1 = (ACC)A[tid + 1], b0 = (ACC)B[tid], b1 = (ACC)B[tid + 1];
+      const ACC P0 = a0 + b0, P1 = a1 + b1, D0 = b0 - a0, D1 = b1 - a1;
+      hP = P0 + P1;
+      dP = P1 - P0;
+      sD = D0 + D1;
+    }
+    ACC yc = yc0;
+#pragma unroll
+    for (int r = 1; r <= BR; ++r) {
+      const T* ra = A + r * kBoxCols + tid;
+      const T* rb = B + r * kBoxCols + tid;
+      const ACC a0 = (ACC)ra[0], a1 = (ACC)ra[1], b0 = (ACC)rb[0], b1 = (ACC)rb[1];
+      const ACC P0 = a0 + b0, P1 = a1 + b1, D0 = b0 - a0, D1 = b1 - a1;
+      const ACC nhP = P0 + P1, ndP = P1 - P0, nsD = D0 + D1;
+      if (r >= r_beg && r <= r_end) {  // grid row gy0 + r - 1, centred y = yc
+        const ACC ex = dP + ndP;
+        const ACC ey = nhP - hP;
+        const ACC et = sD + nsD;
+        const ACC hh = yc * ey;
+        s1 = fma(ex, ex, s1);
+        s2 = fma(ex, ey, s2);
+        s3 = fma(ey, ey, s3);
+        s4 = fma(ex, et, s4);
+        s5 = fma(ey, et, s5);
+        s6 = fma(et, et, s6);
+        u1 = fma(ex, hh, u1);
+        u2 = fma(ey, hh, u2);
+        u3 = fma(hh, et, u3);
+        u4 = fma(hh, hh, u4);
+      }
+      yc += ACC(1);
+      hP = nhP;
+      dP = ndP;
+      sD = nsD;
+    }
+
+    // this thread's ten sums, order m00 m01 m02 m11 m12 m22 r0 r1 r2 et2 (rhs not yet negated)
+    double o[10];
+    if (in_col) {
+      const double S1 = s1, S2 = s2, S3 = s3, S4 = s4, S5 = s5, S6 = s6;
+      const double U1 = u1, U2 = u2, U3 = u3, U4 = u4;
+      o[0] = S1;
+      o[1] = S2;
+      o[2] = fma(xc, S1, U1);
+      o[3] = S3;
+      o[4] = fma(xc, S2, U2);
+      o[5] = fma(xc * xc, S1, fma(2.0 * xc, U1, U4));
+      o[6] = S4;
+      o[7] = S5;
+      o[8] = fma(xc, S4, U3);
+      o[9] = S6;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 10; ++q) o[q] = 0.0;
+    }
+    double* red = S::red_in_buf ? reinterpret_cast<double*>(const_cast<T*>(A))
+                                : reinterpret_cast<double*>(smem + 3 * S::buf_bytes);
+    __syncthreads();  // every thread is done reading A and B for this pair
+#pragma unroll
+    for (int q = 0; q < 10; ++q) red[q * kThreads + tid] = o[q];
+    __syncthreads();
+    if (tid < 10 * kRedSeg) {  // stage 1: value q, segment g sums threads g, g+16, ..., g+240
+      const int q = tid / kRedSeg, g = tid % kRedSeg;
+      const double* rq = red + q * kThreads + g;
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < kThreads / kRedSeg; ++j) acc += rq[j * kRedSeg];
+      part[q * kRedSeg + g] = acc;
+    }
+    __syncthreads();  // scratch consumed: buffer i%3 may be refilled
+    if (a.use_tma) {
+      if (i + 3 < nload) issue(i + 3);
+    } else if (i + 2 < nload) {
+      issue(i + 2);  // buffer (i+2)%3 last held frame p0+i-1
+    }
+    if (tid < 10) {
+      double acc = 0.0;
+#pragma unroll
+      for (int g = 0; g < kRedSeg; ++g) acc += part[tid * kRedSeg + g];
+      acc *= 0.0625;  // undo the 4x stencil scaling of both factors
+      // rhs entries are the negated sums (ttc.py:119)
+      a.partials[((v * n_pairs + p) * a.units + unit) * 10 + tid] = (tid >= 6 && tid <= 8) ? -acc : acc;
+    }
+    if (!a.use_tma) __syncthreads();
+  }
+}
+
+__global__ void moments_finalize_kernel(const double* partials, int64_t n_sys, int units, double count,
+                                        double* sums) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n_sys * 11) return;
+  const int64_t sys = i / 11;
+  const int q = (int)(i - sys * 11);
+  if (q == 10) {
+    sums[i] = count;
+    return;
+  }
+  const double* p = partials + sys * units * 10 + q;
+  double acc = 0.0;
+  for (int u = 0; u < units; ++u) acc += p[(int64_t)u * 10];
+  sums[i] = acc;
+}
+
+template <typename T>
+constexpr int band_rows() {
+  return 16;
+}
+
+struct Plan {
+  int n_bands, n_ctiles, units, chunk, n_chunks, tile_cols;
+};
+
+template <typename T>
+Plan make_plan(int64_t n_videos, int n_frames, int h, int w) {
+  Plan p{};
+  constexpr int BR = band_rows<T>();
+  const int gh = h - 1, gw = w - 1;
+  p.n_bands = (gh + BR - 1) / BR;
+  p.tile_cols = gw <= kTileGridCols ? kTileGridCols : kTileStrideMulti;
+  p.n_ctiles = (gw + p.tile_cols - 1) / p.tile_cols;
+  p.units = p.n_bands * p.n_ctiles;
+  const int n_pairs = n_frames - 1;
+  // ~4 waves of resident CTAs (2 per SM), but >= 8 pairs per CTA so the
+  // one-frame time halo of each chunk stays small
+  const int64_t target = (int64_t)num_sms() * 2 * 4;
+  const int64_t per_chunk = std::max<int64_t>(1, (int64_t)p.units * n_videos);
+  int64_t chunks = std::max<int64_t>(1, (target + per_chunk - 1) / per_chunk);
+  chunks = std::min<int64_t>(chunks, std::max(1, n_pairs / 8));
+  chunks = std::max<int64_t>(1, std::min<int64_t>(chunks, n_pairs));
+  p.chunk = (int)((n_pairs + chunks - 1) / chunks);
+  p.n_chunks = (n_pairs + p.chunk - 1) / p.chunk;
+  return p;
+}
+
+template <typename T>
+size_t ws_bytes(int64_t n_videos, int n_frames, int h, int w) {
+  if (n_frames < 2 || h < 2 || w < 2) return 0;
+  const Plan p = make_plan<T>(n_videos, n_frames, h, w);
+  return (size_t)n_videos * (n_frames - 1) * p.units * 10 * sizeof(double);
+}
+
+template <typename T>
+int launch(const T* frames, int64_t n_videos, int n_frames, int h, int w, int border, double* sums, void* ws,
+           size_t ws_size, cudaStream_t st) {
+  const int n_pairs = n_frames - 1;
+  if (n_pairs <= 0 || n_videos == 0) return CT_OK;
+  constexpr int BR = band_rows<T>();
+  const Plan p = make_plan<T>(n_videos, n_frames, h, w);
+  const size_t need = ws_bytes<T>(n_videos, n_frames, h, w);
+  CT_REQUIRE(ws != nullptr && ws_size >= need, "moments workspace too small (%zu < %zu)", ws_size, need);
+  CT_REQUIRE(n_videos <= 65535 && p.n_chunks <= 65535, "too many videos/chunks for one launch");
+  MomentArgs a{};
+  a.frames = frames;
+  a.partials = reinterpret_cast<double*>(ws);
+  a.n_videos = n_videos;
+  a.n_frames = n_frames;
+  a.h = h;
+  a.w = w;
+  a.gh = h - 1;
+  a.gw = w - 1;
+  a.border = border;
+  a.n_ctiles = p.n_ctiles;
+  a.units = p.units;
+  a.chunk = p.chunk;
+  a.tile_cols = p.tile_cols;
+  CUtensorMap tmap;
+  memset(&tmap, 0, sizeof(tmap));
+  static const bool no_tma = getenv("CT_NO_TMA") != nullptr;  // debugging switch: force the LDG loader
+  a.use_tma = !no_tma && encode_tmap_2d(&tmap, frames, sizeof(T), (uint64_t)w,
+                                        (uint64_t)(n_videos * n_frames * (int64_t)h), kBoxCols, BR + 1);
+  using S = Smem<T, BR>;
+  auto kern = ttc_moments_kernel<T, BR>;
+  CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::total));
+  dim3 grid((unsigned)p.units, (unsigned)p.n_chunks, (unsigned)n_videos);
+  kern<<<grid, kThreads, S::total, st>>>(a, tmap);
+  int rc = check_launch("ttc_moments");
+  if (rc) return rc;
+  const int64_t n_sys = n_videos * n_pairs;
+  const double count = (double)(h - 1 - 2 * border) * (double)(w - 1 - 2 * border);
+  moments_finalize_kernel<<<(unsigned)cdiv(n_sys * 11, 256), 256, 0, st>>>(a.partials, n_sys, p.units, count, sums);
+  return check_launch("moments_finalize");
+}
+
+}  // namespace
+
+size_t moments_workspace(int dtype, int64_t n_videos, int n_frames, int h, int w) {
+  return dtype == CT_F64 ? ws_bytes<double>(n_videos, n_frames, h, w) : ws_bytes<float>(n_videos, n_frames, h, w);
+}
+
+int moments_launch(int dtype, const void* frames, int64_t n_videos, int n_frames, int h, int w, int border,
+                   double* sums, void* ws, size_t ws_size, cudaStream_t st) {
+  if (dtype == CT_F64)
+    return launch<double>((const double*)frames, n_videos, n_frames, h, w, border, sums, ws, ws_size, st);
+  return launch<float>((const float*)frames, n_videos, n_frames, h, w, border, sums, ws, ws_size, st);
+}
+
+int partials_finalize(const double* partials, int64_t n_sys, int units, double count, double* sums,
+                      cudaStream_t st) {
+  if (n_sys == 0) return CT_OK;
+  moments_finalize_kernel<<<(unsigned)cdiv(n_sys * 11, 256), 256, 0, st>>>(partials, n_sys, units, count, sums);
+  return check_launch("moments_finalize");
+}
+
+}  // namespace ct

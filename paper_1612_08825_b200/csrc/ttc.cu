@@ -28,273 +28,15 @@
 #include <algorithm>
 
 #include "common.cuh"
-#include "tma.cuh"
+#include "moments.cuh"
 
 namespace ct {
 namespace {
-
-template <typename T>
-struct AccT;
-template <>
-struct AccT<double> {
-  using type = double;
-};
-template <>
-struct AccT<float> {
-  using type = float;
-};
-
-constexpr int kBoxCols = 256;     // frame columns per tile (TMA box inner extent)
-constexpr int kTileGridCols = 255;  // grid columns of a single-tile frame (w <= 256)
-// With several column tiles the tile stride is 252 grid columns: tile starts
-// must be 16-byte aligned for the TMA box (multiple of 4 f32 / 2 f64
-// elements); a box start at element 255 raises an illegal-instruction fault.
-constexpr int kTileStrideMulti = 252;
-constexpr int kMomThreads = 128;  // 2 grid columns per thread
-
-struct MomentArgs {
-  const void* frames;
-  double* partials;  // [n_videos][n_pairs][units][10]
-  int64_t n_videos;
-  int n_frames;
-  int h, w, gh, gw, border;
-  int band_rows;
-  int n_bands, n_ctiles, units;
-  int chunk;  // pairs per CTA
-  int use_tma;
-  int tile_cols;  // grid columns per tile (255 single tile, 252 otherwise)
-};
-
-template <typename T>
-__host__ __device__ constexpr size_t band_buf_elems(int band_rows) {
-  // rows x 256 columns, +8 elements so the last thread's right-neighbour
-  // vector read stays inside the buffer (those lanes are masked)
-  return (size_t)(band_rows + 1) * kBoxCols + 8;
-}
-
-template <typename T>
-__host__ __device__ size_t band_buf_bytes(int band_rows) {
-  return (band_buf_elems<T>(band_rows) * sizeof(T) + 127) & ~size_t(127);
-}
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
-}
-
-template <typename T>
-__global__ void __launch_bounds__(kMomThreads) ttc_moments_kernel(const MomentArgs a,
-                                                                   const __grid_constant__ CUtensorMap tmap) {
-  using ACC = typename AccT<T>::type;
-  extern __shared__ __align__(128) unsigned char smem[];
-  const int BR = a.band_rows;
-  const size_t bbytes = band_buf_bytes<T>(BR);
-  T* bufs[3] = {reinterpret_cast<T*>(smem), reinterpret_cast<T*>(smem + bbytes),
-                reinterpret_cast<T*>(smem + 2 * bbytes)};
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 3 * bbytes);
-  double* red = reinterpret_cast<double*>(smem + 3 * bbytes + 64);  // [2][4 warps][10]
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int unit = blockIdx.x;
-  const int band = unit / a.n_ctiles, ctile = unit - band * a.n_ctiles;
-  const int gy0 = band * BR;                 // first grid row (== first frame row) of the band
-  const int cx0 = ctile * a.tile_cols;        // first grid column (== first frame column)
-  const int64_t v = blockIdx.z;
-  const int n_pairs = a.n_frames - 1;
-  const int p0 = blockIdx.y * a.chunk;
-  const int p1 = min(p0 + a.chunk, n_pairs);  // pairs [p0, p1) -> frames p0..p1
-  if (p0 >= p1) return;
-  const int nload = p1 - p0 + 1;
-  const uint32_t box_bytes = (uint32_t)((BR + 1) * kBoxCols * sizeof(T));
-
-  // this thread's two grid columns (local 2*tid, 2*tid+1)
-  const int lc = 2 * tid;
-  const int gxa = cx0 + lc, gxb = gxa + 1;
-  const bool ina = lc < a.tile_cols && gxa >= a.border && gxa < a.gw - a.border;
-  const bool inb = lc + 1 < a.tile_cols && gxb >= a.border && gxb < a.gw - a.border;
-  const ACC xa = (ACC)((double)gxa - (double)(a.gw - 1) / 2.0);
-  const ACC xb = (ACC)((double)gxb - (double)(a.gw - 1) / 2.0);
-  const double ycen = (double)(a.gh - 1) / 2.0;
-  const int64_t row0 = (v * a.n_frames) * (int64_t)a.h + gy0;  // frame p's band row = row0 + p*h
-
-  auto issue = [&](int f) {  // frame p0+f -> buffer f%3
-    T* dst = bufs[f % 3];
-    if (a.use_tma) {
-      if (tid == 0) {
-        mbar_arrive_expect_tx(&bars[f % 3], box_bytes);
-        tma_load_2d(dst, &tmap, &bars[f % 3], cx0, (int)(row0 + (int64_t)(p0 + f) * a.h));
-      }
-    } else {
-      const T* src = reinterpret_cast<const T*>(a.frames) + (row0 + (int64_t)(p0 + f) * a.h) * a.w;
-      const int64_t rows_left = (int64_t)a.n_videos * a.n_frames * a.h - (row0 + (int64_t)(p0 + f) * a.h);
-      for (int idx = tid; idx < (BR + 1) * kBoxCols; idx += kMomThreads) {
-        const int r = idx / kBoxCols, c = idx - r * kBoxCols;
-        T val = T(0);
-        if (r < rows_left && cx0 + c < a.w) val = src[(int64_t)r * a.w + cx0 + c];
-        dst[idx] = val;
-      }
-    }
-  };
-
-  if (a.use_tma) {
-    if (tid == 0) {
-      for (int i = 0; i < 3; ++i) mbar_init(&bars[i], 1);
-      mbar_fence_init();
-    }
-    __syncthreads();
-    for (int f = 0; f < min(3, nload); ++f) issue(f);
-  } else {
-    issue(0);
-    issue(1);
-    __syncthreads();
-  }
-
-  for (int i = 0; i < p1 - p0; ++i) {
-    const int p = p0 + i;
-    if (a.use_tma) {
-      mbar_wait(&bars[i % 3], (uint32_t)((i / 3) & 1));
-      mbar_wait(&bars[(i + 1) % 3], (uint32_t)(((i + 1) / 3) & 1));
-    }
-    const T* A = bufs[i % 3];
-    const T* B = bufs[(i + 1) % 3];
-
-    // per-column accumulators: S1..S6 = Ex^2 ExEy Ey^2 ExEt EyEt Et^2, U1..U4 = ExH EyH HEt HH
-    ACC s[2][10];
-#pragma unroll
-    for (int c = 0; c < 2; ++c)
-#pragma unroll
-      for (int q = 0; q < 10; ++q) s[c][q] = ACC(0);
-
-    ACC hP[2], dP[2], sD[2];
-    {
-      // frame row 0 of the band
-      const T* ra = A + lc;
-      const T* rb = B + lc;
-      ACC pa[3], pd[3];
-#pragma unroll
-      for (int e = 0; e < 3; ++e) {
-        const ACC x0 = (ACC)ra[e], x1 = (ACC)rb[e];
-        pa[e] = x0 + x1;
-        pd[e] = x1 - x0;
-      }
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        hP[c] = pa[c] + pa[c + 1];
-        dP[c] = pa[c + 1] - pa[c];
-        sD[c] = pd[c] + pd[c + 1];
-      }
-    }
-    const int r_end = min(BR, a.gh - a.border - gy0);  // last grid row (exclusive, band-local) + 1
-    const int r_beg = max(1, a.border - gy0 + 1);       // frame row index whose grid row is >= border
-#pragma unroll 2
-    for (int r = 1; r <= BR; ++r) {
-      const T* ra = A + r * kBoxCols + lc;
-      const T* rb = B + r * kBoxCols + lc;
-      ACC pa[3], pd[3];
-#pragma unroll
-      for (int e = 0; e < 3; ++e) {
-        const ACC x0 = (ACC)ra[e], x1 = (ACC)rb[e];
-        pa[e] = x0 + x1;
-        pd[e] = x1 - x0;
-      }
-      ACC nhP[2], ndP[2], nsD[2];
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        nhP[c] = pa[c] + pa[c + 1];
-        ndP[c] = pa[c + 1] - pa[c];
-        nsD[c] = pd[c] + pd[c + 1];
-      }
-      // grid row gy = gy0 + r - 1
-      if (r >= r_beg && r <= r_end) {
-        const ACC yc = (ACC)((double)(gy0 + r - 1) - ycen);
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          const ACC ex = dP[c] + ndP[c];
-          const ACC ey = nhP[c] - hP[c];
-          const ACC et = sD[c] + nsD[c];
-          const ACC hh = yc * ey;
-          s[c][0] = fma(ex, ex, s[c][0]);
-          s[c][1] = fma(ex, ey, s[c][1]);
-          s[c][2] = fma(ey, ey, s[c][2]);
-          s[c][3] = fma(ex, et, s[c][3]);
-          s[c][4] = fma(ey, et, s[c][4]);
-          s[c][5] = fma(et, et, s[c][5]);
-          s[c][6] = fma(ex, hh, s[c][6]);
-          s[c][7] = fma(ey, hh, s[c][7]);
-          s[c][8] = fma(hh, et, s[c][8]);
-          s[c][9] = fma(hh, hh, s[c][9]);
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        hP[c] = nhP[c];
-        dP[c] = ndP[c];
-        sD[c] = nsD[c];
-      }
-    }
-
-    // combine the columns: ten sums in the order m00 m01 m02 m11 m12 m22 r0 r1 r2 et2
-    double out[10];
-#pragma unroll
-    for (int q = 0; q < 10; ++q) out[q] = 0.0;
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      const bool on = c == 0 ? ina : inb;
-      if (!on) continue;
-      const double xc = (double)(c == 0 ? xa : xb);
-      const double S1 = s[c][0], S2 = s[c][1], S3 = s[c][2], S4 = s[c][3], S5 = s[c][4], S6 = s[c][5];
-      const double U1 = s[c][6], U2 = s[c][7], U3 = s[c][8], U4 = s[c][9];
-      out[0] += S1;                                   // sum Ex^2
-      out[1] += S2;                                   // sum Ex Ey
-      out[2] += fma(xc, S1, U1);                      // sum Ex G
-      out[3] += S3;                                   // sum Ey^2
-      out[4] += fma(xc, S2, U2);                      // sum Ey G
-      out[5] += fma(xc * xc, S1, fma(2.0 * xc, U1, U4));  // sum G^2
-      out[6] += S4;                                   // sum Ex Et
-      out[7] += S5;                                   // sum Ey Et
-      out[8] += fma(xc, S4, U3);                      // sum G Et
-      out[9] += S6;                                   // sum Et^2
-    }
-#pragma unroll
-    for (int q = 0; q < 10; ++q) out[q] = warp_sum(out[q]);
-    double* rb = red + (i & 1) * 40;
-    if (lane == 0) {
-#pragma unroll
-      for (int q = 0; q < 10; ++q) rb[warp * 10 + q] = out[q];
-    }
-    __syncthreads();  // red written; buffers of frame p0+i fully consumed
-    if (a.use_tma) {
-      if (i + 3 < nload) {
-        if (tid == 0) fence_proxy_async_smem();
-        issue(i + 3);
-      }
-    } else if (i + 2 < nload) {
-      issue(i + 2);  // buffer (i+2)%3 last held frame p0+i-1
-    }
-    if (tid < 10) {
-      const double t = ((rb[tid] + rb[10 + tid]) + (rb[20 + tid] + rb[30 + tid])) * 0.0625;
-      // rhs entries are negated sums (ttc.py:119)
-      a.partials[((v * n_pairs + p) * a.units + unit) * 10 + tid] = (tid >= 6 && tid <= 8) ? -t : t;
-    }
-    if (!a.use_tma) __syncthreads();
-  }
-}
-
-__global__ void moments_finalize_kernel(const double* partials, int64_t n_sys, int units, double count,
-                                        double* sums) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n_sys * 11) return;
-  const int64_t sys = i / 11;
-  const int q = (int)(i - sys * 11);
-  if (q == 10) {
-    sums[i] = count;
-    return;
-  }
-  const double* p = partials + sys * units * 10 + q;
-  double acc = 0.0;
-  for (int u = 0; u < units; ++u) acc += p[(int64_t)u * 10];
-  sums[i] = acc;
 }
 
 // ------------------------------------------------------------ fields ------
@@ -555,96 +297,6 @@ __global__ void __launch_bounds__(256) pyramid_down_kernel(const T* __restrict__
 // ------------------------------------------------------------- host -------
 
 template <typename T>
-int band_rows_for() {
-  static const int env_rows = getenv("CT_BAND_ROWS") ? atoi(getenv("CT_BAND_ROWS")) : 0;  // tuning switch
-  if (env_rows > 0) return env_rows;
-  return sizeof(T) == 8 ? 16 : 32;
-}
-
-template <typename T>
-size_t moments_smem_bytes(int br) {
-  return 3 * band_buf_bytes<T>(br) + 64 + 2 * 40 * sizeof(double);
-}
-
-struct MomentPlan {
-  int band_rows, n_bands, n_ctiles, units, chunk, n_chunks, tile_cols;
-};
-
-template <typename T>
-MomentPlan plan_moments(int64_t n_videos, int n_frames, int h, int w) {
-  MomentPlan p{};
-  p.band_rows = band_rows_for<T>();
-  const int gh = h - 1, gw = w - 1;
-  p.n_bands = (gh + p.band_rows - 1) / p.band_rows;
-  p.tile_cols = gw <= kTileGridCols ? kTileGridCols : kTileStrideMulti;
-  p.n_ctiles = (gw + p.tile_cols - 1) / p.tile_cols;
-  p.units = p.n_bands * p.n_ctiles;
-  const int n_pairs = n_frames - 1;
-  // enough CTAs for ~4 waves at 2 CTAs/SM, but at least 8 pairs per CTA so
-  // the one-frame halo of each time chunk stays a small overhead
-  const int64_t target = (int64_t)num_sms() * 2 * 4;
-  const int64_t per_chunk = std::max<int64_t>(1, (int64_t)p.units * n_videos);
-  int64_t chunks = std::max<int64_t>(1, (target + per_chunk - 1) / per_chunk);
-  chunks = std::min<int64_t>(chunks, std::max(1, n_pairs / 8));
-  chunks = std::max<int64_t>(1, std::min<int64_t>(chunks, n_pairs));
-  p.chunk = (int)((n_pairs + chunks - 1) / chunks);
-  p.n_chunks = (n_pairs + p.chunk - 1) / p.chunk;
-  return p;
-}
-
-template <typename T>
-size_t moments_ws_bytes(int64_t n_videos, int n_frames, int h, int w) {
-  if (n_frames < 2 || h < 2 || w < 2) return 0;
-  MomentPlan p = plan_moments<T>(n_videos, n_frames, h, w);
-  return (size_t)n_videos * (n_frames - 1) * p.units * 10 * sizeof(double);
-}
-
-template <typename T>
-int launch_moments(const T* frames, int64_t n_videos, int n_frames, int h, int w, int border, double* sums,
-                   void* ws, size_t ws_bytes, cudaStream_t st) {
-  const int n_pairs = n_frames - 1;
-  if (n_pairs <= 0 || n_videos == 0) return CT_OK;
-  MomentPlan p = plan_moments<T>(n_videos, n_frames, h, w);
-  const size_t need = moments_ws_bytes<T>(n_videos, n_frames, h, w);
-  CT_REQUIRE(ws != nullptr && ws_bytes >= need, "moments workspace too small (%zu < %zu)", ws_bytes, need);
-  MomentArgs a{};
-  a.frames = frames;
-  a.partials = reinterpret_cast<double*>(ws);
-  a.n_videos = n_videos;
-  a.n_frames = n_frames;
-  a.h = h;
-  a.w = w;
-  a.gh = h - 1;
-  a.gw = w - 1;
-  a.border = border;
-  a.band_rows = p.band_rows;
-  a.n_bands = p.n_bands;
-  a.n_ctiles = p.n_ctiles;
-  a.units = p.units;
-  a.chunk = p.chunk;
-  a.tile_cols = p.tile_cols;
-  CUtensorMap tmap;
-  memset(&tmap, 0, sizeof(tmap));
-  static const bool no_tma = getenv("CT_NO_TMA") != nullptr;  // debugging switch
-  a.use_tma = !no_tma && encode_tmap_2d(&tmap, frames, sizeof(T), (uint64_t)w, (uint64_t)(n_videos * n_frames * (int64_t)h),
-                             kBoxCols, p.band_rows + 1)
-                  ? 1
-                  : 0;
-  const size_t smem = moments_smem_bytes<T>(p.band_rows);
-  auto kern = ttc_moments_kernel<T>;
-  CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  CT_REQUIRE(n_videos <= 65535 && p.n_chunks <= 65535, "too many videos/chunks for one launch");
-  dim3 grid((unsigned)p.units, (unsigned)p.n_chunks, (unsigned)n_videos);
-  kern<<<grid, kMomThreads, smem, st>>>(a, tmap);
-  int rc = check_launch("ttc_moments");
-  if (rc) return rc;
-  const int64_t n_sys = n_videos * n_pairs;
-  const double count = (double)(h - 1 - 2 * border) * (double)(w - 1 - 2 * border);
-  moments_finalize_kernel<<<(unsigned)cdiv(n_sys * 11, 256), 256, 0, st>>>(a.partials, n_sys, p.units, count, sums);
-  return check_launch("moments_finalize");
-}
-
-template <typename T>
 int launch_pyramid(const T* in, int64_t n_images, int h, int w, T* out, cudaStream_t st) {
   const int dh = h / 2, dw = w / 2;
   if (n_images == 0 || dh == 0 || dw == 0) return CT_OK;
@@ -691,7 +343,7 @@ size_t run_seq_ws(int64_t nv, int nf, int h, int w, int level, int max_level) {
       lw /= 2;
       continue;
     }
-    mom = std::max(mom, moments_ws_bytes<T>(nv, nf, lh, lw));
+    mom = std::max(mom, moments_workspace(sizeof(T) == 8 ? CT_F64 : CT_F32, nv, nf, lh, lw));
     lh /= 2;
     lw /= 2;
   }
@@ -734,13 +386,13 @@ int run_seq(const T* frames, int64_t nv, int nf, int h, int w, int level, int ma
   }
   size_t mom = 0;
   for (int l = 0; l < nl; ++l)
-    if (ms || l == level) mom = std::max(mom, moments_ws_bytes<T>(nv, nf, level_h[l], level_w[l]));
+    if (ms || l == level) mom = std::max(mom, moments_workspace(sizeof(T) == 8 ? CT_F64 : CT_F32, nv, nf, level_h[l], level_w[l]));
   void* mom_ws = cur;
   cur += align256(mom);
   double* sums = reinterpret_cast<double*>(cur);
   cur += align256((size_t)np * 11 * sizeof(double));
   if (!ms) {
-    int rc = launch_moments<T>(level_ptr[level], nv, nf, level_h[level], level_w[level], 1, sums, mom_ws, mom, st);
+    int rc = moments_launch(sizeof(T) == 8 ? CT_F64 : CT_F32, level_ptr[level], nv, nf, level_h[level], level_w[level], 1, sums, mom_ws, mom, st);
     if (rc) return rc;
     return launch_solve(sums, np, c_min, level, est, 10, st);
   }
@@ -750,7 +402,7 @@ int run_seq(const T* frames, int64_t nv, int nf, int h, int w, int level, int ma
   }
   double* est_levels = reinterpret_cast<double*>(cur);
   for (int l = 0; l < nl; ++l) {
-    int rc = launch_moments<T>(level_ptr[l], nv, nf, level_h[l], level_w[l], 1, sums, mom_ws, mom, st);
+    int rc = moments_launch(sizeof(T) == 8 ? CT_F64 : CT_F32, level_ptr[l], nv, nf, level_h[l], level_w[l], 1, sums, mom_ws, mom, st);
     if (rc) return rc;
     rc = launch_solve(sums, np, c_min, l, est_levels + l * 10, (int64_t)nl * 10, st);
     if (rc) return rc;
@@ -830,14 +482,12 @@ extern "C" int ct_normal_system(int dtype, const void* ex, const void* ey, const
   int rc = check_launch("normal_system");
   if (rc) return rc;
   const double count = (double)(gh - 2 * border) * (double)(gw - 2 * border);
-  moments_finalize_kernel<<<1, 32, 0, st>>>(partials, 1, kNsBlocks, count, sums);
-  return check_launch("normal_system_finalize");
+  return partials_finalize(partials, 1, kNsBlocks, count, sums, st);
 }
 
 extern "C" size_t ct_ttc_moments_workspace_bytes(int dtype, int64_t n_videos, int64_t n_frames, int64_t h,
                                                  int64_t w) {
-  if (dtype == CT_F64) return moments_ws_bytes<double>(n_videos, (int)n_frames, (int)h, (int)w);
-  return moments_ws_bytes<float>(n_videos, (int)n_frames, (int)h, (int)w);
+  return moments_workspace(dtype, n_videos, (int)n_frames, (int)h, (int)w);
 }
 
 extern "C" int ct_ttc_moments(int dtype, const void* frames, int64_t n_videos, int64_t n_frames, int64_t h,
@@ -847,12 +497,8 @@ extern "C" int ct_ttc_moments(int dtype, const void* frames, int64_t n_videos, i
   CT_REQUIRE(n_frames >= 2, "need at least two frames");
   CT_REQUIRE(h >= 4 && w >= 4, "frames of (%lld, %lld) leave no interior, need >= 4", (long long)h, (long long)w);
   CT_REQUIRE(h < (1 << 30) && w < (1 << 30) && n_frames < (1 << 30) && n_videos >= 0, "bad extents");
-  cudaStream_t st = as_stream(stream);
-  if (dtype == CT_F64)
-    return launch_moments<double>((const double*)frames, n_videos, (int)n_frames, (int)h, (int)w, 1, sums, workspace,
-                                  workspace_bytes, st);
-  return launch_moments<float>((const float*)frames, n_videos, (int)n_frames, (int)h, (int)w, 1, sums, workspace,
-                               workspace_bytes, st);
+  return moments_launch(dtype, frames, n_videos, (int)n_frames, (int)h, (int)w, 1, sums, workspace, workspace_bytes,
+                        as_stream(stream));
 }
 
 extern "C" int ct_ttc_solve(const double* sums, int64_t count, double c_min, int level, double* est, void* stream) {
