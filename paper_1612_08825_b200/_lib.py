@@ -13,7 +13,8 @@ import os
 import numpy as np
 import torch
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libconvtact_b200.so")
+# CT_LIB_PATH points at an alternative build (A/B tuning runs only)
+LIB_PATH = os.environ.get("CT_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libconvtact_b200.so")
 
 CT_OK, CT_EINVAL, CT_ECUDA, CT_EUNSUPPORTED = 0, 1, 2, 3
 CT_F64, CT_F32 = 0, 1

@@ -20,7 +20,8 @@
 //     (fixed column, fixed xc) accumulates S = {Ex^2, ExEy, Ey^2, ExEt, EyEt,
 //     Et^2} and U = {Ex H, Ey H, H Et, H H}; then sum(Ex G) = xc S1 + U1,
 //     sum(Ey G) = xc S2 + U2, sum(G Et) = xc S4 + U3, sum(G^2) = xc^2 S1 +
-//     2 xc U1 + U4.  ~21 FP64 ops per grid pixel.
+//     2 xc U1 + U4, with the U sums accumulated under band-relative y
+//     weights (see sweep()); ~21 FP64 ops per grid pixel.
 //   * Per pair the 256 per-thread sums are reduced through shared memory in
 //     a fixed tree (the dead previous-frame buffer is the scratch), giving one
 //     partial per band; moments_finalize adds the band partials in a fixed
@@ -77,6 +78,60 @@ struct Smem {
   static constexpr size_t total = part_off + 10 * kRedSeg * sizeof(double);
 };
 
+// One thread's sweep down its column of the band for one frame pair (A, B):
+// m = {S1..S6, U1'..U4'} over the grid rows whose band-local frame row r lies
+// in [r_beg, r_end].  The y weights are relative to the band's first grid row
+// (w = r - 1, a compile-time constant per unrolled row), so row 1 needs no U
+// terms and no running coordinate is carried; the caller shifts them by the
+// absolute coordinate yc0 of that row: U1 = yc0 S2 + U1', U2 = yc0 S3 + U2',
+// U3 = yc0 S5 + U3', U4 = yc0^2 S3 + 2 yc0 U2' + U4'.
+// CHECK=false is the interior fast path (all rows, no per-row tests).
+template <typename T, int BR, bool CHECK>
+__device__ __forceinline__ void sweep(const T* __restrict__ A, const T* __restrict__ B, int col, int r_beg,
+                                      int r_end, typename AccT<T>::type (&m)[10]) {
+  using ACC = typename AccT<T>::type;
+  ACC s1 = 0, s2 = 0, s3 = 0, s4 = 0, s5 = 0, s6 = 0, u1 = 0, u2 = 0, u3 = 0, u4 = 0;
+  ACC hP, dP, sD;
+  {
+    const ACC a0 = (ACC)A[col], a1 = (ACC)A[col + 1], b0 = (ACC)B[col], b1 = (ACC)B[col + 1];
+    const ACC P0 = a0 + b0, P1 = a1 + b1, D0 = b0 - a0, D1 = b1 - a1;
+    hP = P0 + P1;
+    dP = P1 - P0;
+    sD = D0 + D1;
+  }
+#pragma unroll
+  for (int r = 1; r <= BR; ++r) {
+    const T* ra = A + r * kBoxCols + col;
+    const T* rb = B + r * kBoxCols + col;
+    const ACC a0 = (ACC)ra[0], a1 = (ACC)ra[1], b0 = (ACC)rb[0], b1 = (ACC)rb[1];
+    const ACC P0 = a0 + b0, P1 = a1 + b1, D0 = b0 - a0, D1 = b1 - a1;
+    const ACC nhP = P0 + P1, ndP = P1 - P0, nsD = D0 + D1;
+    if (!CHECK || (r >= r_beg && r <= r_end)) {  // grid row gy0 + r - 1
+      const ACC ex = dP + ndP;
+      const ACC ey = nhP - hP;
+      const ACC et = sD + nsD;
+      s1 = fma(ex, ex, s1);
+      s2 = fma(ex, ey, s2);
+      s3 = fma(ey, ey, s3);
+      s4 = fma(ex, et, s4);
+      s5 = fma(ey, et, s5);
+      s6 = fma(et, et, s6);
+      if (r >= 2) {
+        const ACC hh = r == 2 ? ey : ACC(r - 1) * ey;
+        u1 = fma(ex, hh, u1);
+        u2 = fma(ey, hh, u2);
+        u3 = fma(hh, et, u3);
+        u4 = fma(hh, hh, u4);
+      }
+    }
+    hP = nhP;
+    dP = ndP;
+    sD = nsD;
+  }
+  m[0] = s1; m[1] = s2; m[2] = s3; m[3] = s4; m[4] = s5;
+  m[5] = s6; m[6] = u1; m[7] = u2; m[8] = u3; m[9] = u4;
+}
+
 template <typename T, int BR>
 __global__ void __launch_bounds__(kThreads, 2) ttc_moments_kernel(const MomentArgs a,
                                                                   const __grid_constant__ CUtensorMap tmap) {
@@ -103,8 +158,8 @@ __global__ void __launch_bounds__(kThreads, 2) ttc_moments_kernel(const MomentAr
   const int gx = cx0 + tid;
   const bool in_col = tid < a.tile_cols && gx >= a.border && gx < a.gw - a.border;
   const double xc = (double)gx - (double)(a.gw - 1) / 2.0;
-  const ACC yc0 = (ACC)((double)gy0 - (double)(a.gh - 1) / 2.0);  // centred y of grid row gy0
-  const int64_t row0 = (v * a.n_frames) * (int64_t)a.h + gy0;     // band row of frame p: row0 + p*h
+  const double yc0 = (double)gy0 - (double)(a.gh - 1) / 2.0;    // centred y of grid row gy0
+  const int64_t row0 = (v * a.n_frames) * (int64_t)a.h + gy0;  // band row of frame p: row0 + p*h
   // band-local frame-row range r in [r_beg, r_end] whose grid row gy0 + r - 1 is interior
   const int r_end = min(BR, a.gh - a.border - gy0);
   const int r_beg = max(1, a.border - gy0 + 1);
@@ -152,50 +207,20 @@ __global__ void __launch_bounds__(kThreads, 2) ttc_moments_kernel(const MomentAr
     const T* A = buf(i % 3);
     const T* B = buf((i + 1) % 3);
 
-    ACC s1 = 0, s2 = 0, s3 = 0, s4 = 0, s5 = 0, s6 = 0, u1 = 0, u2 = 0, u3 = 0, u4 = 0;
-    ACC hP, dP, sD;
-    {
-      const ACC a0 = (ACC)A[tid], a1 = (ACC)A[tid + 1], b0 = (ACC)B[tid], b1 = (ACC)B[tid + 1];
-      const ACC P0 = a0 + b0, P1 = a1 + b1, D0 = b0 - a0, D1 = b1 - a1;
-      hP = P0 + P1;
-      dP = P1 - P0;
-      sD = D0 + D1;
-    }
-    ACC yc = yc0;
-#pragma unroll
-    for (int r = 1; r <= BR; ++r) {
-      const T* ra = A + r * kBoxCols + tid;
-      const T* rb = B + r * kBoxCols + tid;
-      const ACC a0 = (ACC)ra[0], a1 = (ACC)ra[1], b0 = (ACC)rb[0], b1 = (ACC)rb[1];
-      const ACC P0 = a0 + b0, P1 = a1 + b1, D0 = b0 - a0, D1 = b1 - a1;
-      const ACC nhP = P0 + P1, ndP = P1 - P0, nsD = D0 + D1;
-      if (r >= r_beg && r <= r_end) {  // grid row gy0 + r - 1, centred y = yc
-        const ACC ex = dP + ndP;
-        const ACC ey = nhP - hP;
-        const ACC et = sD + nsD;
-        const ACC hh = yc * ey;
-        s1 = fma(ex, ex, s1);
-        s2 = fma(ex, ey, s2);
-        s3 = fma(ey, ey, s3);
-        s4 = fma(ex, et, s4);
-        s5 = fma(ey, et, s5);
-        s6 = fma(et, et, s6);
-        u1 = fma(ex, hh, u1);
-        u2 = fma(ey, hh, u2);
-        u3 = fma(hh, et, u3);
-        u4 = fma(hh, hh, u4);
-      }
-      yc += ACC(1);
-      hP = nhP;
-      dP = ndP;
-      sD = nsD;
-    }
+    ACC m[10];
+    if (r_beg <= 1 && r_end >= BR)
+      sweep<T, BR, false>(A, B, tid, 1, BR, m);
+    else
+      sweep<T, BR, true>(A, B, tid, r_beg, r_end, m);
 
     // this thread's ten sums, order m00 m01 m02 m11 m12 m22 r0 r1 r2 et2 (rhs not yet negated)
     double o[10];
     if (in_col) {
-      const double S1 = s1, S2 = s2, S3 = s3, S4 = s4, S5 = s5, S6 = s6;
-      const double U1 = u1, U2 = u2, U3 = u3, U4 = u4;
+      const double S1 = m[0], S2 = m[1], S3 = m[2], S4 = m[3], S5 = m[4], S6 = m[5];
+      const double U1 = fma(yc0, S2, (double)m[6]);
+      const double U2 = fma(yc0, S3, (double)m[7]);
+      const double U3 = fma(yc0, S5, (double)m[8]);
+      const double U4 = fma(yc0 * yc0, S3, fma(2.0 * yc0, (double)m[7], (double)m[9]));
       o[0] = S1;
       o[1] = S2;
       o[2] = fma(xc, S1, U1);
