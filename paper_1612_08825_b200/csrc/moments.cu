@@ -267,25 +267,31 @@ __global__ void __launch_bounds__(kThreads, 2) ttc_moments_kernel(const MomentAr
   }
 }
 
-__global__ void moments_finalize_kernel(const double* partials, int64_t n_sys, int units, double count,
-                                        double* sums) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n_sys * 11) return;
-  const int64_t sys = i / 11;
-  const int q = (int)(i - sys * 11);
-  if (q == 10) {
-    sums[i] = count;
-    return;
+// sums[sys] = fixed-order sum of the `units` band partials of each system.
+// One warp per (system, value): lanes take units lane, lane+32, ... and a
+// butterfly combines them (fixed tree -> deterministic).
+__global__ void __launch_bounds__(320) moments_finalize_kernel(const double* partials, int64_t n_sys, int units,
+                                                               double count, double* sums) {
+  const int q = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t sys = blockIdx.x; sys < n_sys; sys += gridDim.x) {
+    const double* p = partials + sys * units * 10 + q;
+    double acc = 0.0;
+    for (int u = lane; u < units; u += 32) acc += p[(int64_t)u * 10];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) sums[sys * 11 + q] = acc;
+    if (threadIdx.x == 0) sums[sys * 11 + 10] = count;
   }
-  const double* p = partials + sys * units * 10 + q;
-  double acc = 0.0;
-  for (int u = 0; u < units; ++u) acc += p[(int64_t)u * 10];
-  sums[i] = acc;
 }
 
+inline unsigned finalize_grid(int64_t n_sys) { return (unsigned)std::min<int64_t>(n_sys, 65535); }
+
+// Band height: 16 rows for f64 (3 x 35 KB buffers, 2 CTAs/SM, FP64-bound),
+// 32 rows for f32 (3 x 34 KB; the cheaper FP32 math needs bigger TMA
+// transfers and fewer per-pair reductions per pixel).
 template <typename T>
 constexpr int band_rows() {
-  return 16;
+  return sizeof(T) == 8 ? 16 : 32;
 }
 
 struct Plan {
@@ -359,7 +365,7 @@ int launch(const T* frames, int64_t n_videos, int n_frames, int h, int w, int bo
   if (rc) return rc;
   const int64_t n_sys = n_videos * n_pairs;
   const double count = (double)(h - 1 - 2 * border) * (double)(w - 1 - 2 * border);
-  moments_finalize_kernel<<<(unsigned)cdiv(n_sys * 11, 256), 256, 0, st>>>(a.partials, n_sys, p.units, count, sums);
+  moments_finalize_kernel<<<finalize_grid(n_sys), 320, 0, st>>>(a.partials, n_sys, p.units, count, sums);
   return check_launch("moments_finalize");
 }
 
@@ -379,7 +385,7 @@ int moments_launch(int dtype, const void* frames, int64_t n_videos, int n_frames
 int partials_finalize(const double* partials, int64_t n_sys, int units, double count, double* sums,
                       cudaStream_t st) {
   if (n_sys == 0) return CT_OK;
-  moments_finalize_kernel<<<(unsigned)cdiv(n_sys * 11, 256), 256, 0, st>>>(partials, n_sys, units, count, sums);
+  moments_finalize_kernel<<<finalize_grid(n_sys), 320, 0, st>>>(partials, n_sys, units, count, sums);
   return check_launch("moments_finalize");
 }
 

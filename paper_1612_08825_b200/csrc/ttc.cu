@@ -249,39 +249,61 @@ __global__ void multiscale_select_kernel(const double* est_levels, int64_t count
 
 // ------------------------------------------------------------- pyramid ----
 
-constexpr int kPyTile = 32;
+constexpr int kPyTileY = 32, kPyTileX = 64;  // outputs per CTA
+
+template <typename T>
+struct Vec2;
+template <>
+struct Vec2<double> {
+  using type = double2;
+};
+template <>
+struct Vec2<float> {
+  using type = float2;
+};
 
 // downsample (ttc.py:187-204): dec = 0.25*(((f00+f01)+f10)+f11) on the even
 // crop, then the 5x5 binomial over the edge-padded dec, taps row-major with
-// FMA (bit-identical to the reference in float64).
-template <typename T>
+// FMA (bit-identical to the reference in float64).  A CTA stages the
+// (32+4) x (64+4) dec tile (edge-clamped) in shared memory, reading each input
+// pixel pair as one 2-element vector when the row pitch allows (VEC).
+template <typename T, bool VEC>
 __global__ void __launch_bounds__(256) pyramid_down_kernel(const T* __restrict__ in, int64_t n_images, int h,
                                                            int w, T* __restrict__ out) {
-  __shared__ T dec[kPyTile + 4][kPyTile + 4 + 1];
+  constexpr int SY = kPyTileY + 4, SX = kPyTileX + 4;
+  __shared__ T dec[SY][SX + 1];
   const int dh = h / 2, dw = w / 2;
-  const int tiles_x = (dw + kPyTile - 1) / kPyTile;
-  const int ty0 = (blockIdx.x / tiles_x) * kPyTile, tx0 = (blockIdx.x % tiles_x) * kPyTile;
+  const int tiles_x = (dw + kPyTileX - 1) / kPyTileX;
+  const int ty0 = (blockIdx.x / tiles_x) * kPyTileY, tx0 = (blockIdx.x % tiles_x) * kPyTileX;
   const T b5[5] = {T(1.0 / 16.0), T(4.0 / 16.0), T(6.0 / 16.0), T(4.0 / 16.0), T(1.0 / 16.0)};
+  using V2 = typename Vec2<T>::type;
   for (int64_t img = blockIdx.y; img < n_images; img += gridDim.y) {
     const T* src = in + img * (int64_t)h * w;
     __syncthreads();
-    for (int idx = threadIdx.x; idx < (kPyTile + 4) * (kPyTile + 4); idx += blockDim.x) {
-      const int r = idx / (kPyTile + 4), c = idx % (kPyTile + 4);
+    for (int idx = threadIdx.x; idx < SY * SX; idx += blockDim.x) {
+      const int r = idx / SX, c = idx - r * SX;
       const int yy = min(max(ty0 + r - 2, 0), dh - 1), xx = min(max(tx0 + c - 2, 0), dw - 1);
       const T* p0 = src + (int64_t)(2 * yy) * w + 2 * xx;
       const T* p1 = p0 + w;
+      T f00, f01, f10, f11;
+      if (VEC) {
+        const V2 u = *reinterpret_cast<const V2*>(p0), l = *reinterpret_cast<const V2*>(p1);
+        f00 = u.x; f01 = u.y; f10 = l.x; f11 = l.y;
+      } else {
+        f00 = p0[0]; f01 = p0[1]; f10 = p1[0]; f11 = p1[1];
+      }
       T s;
       if constexpr (sizeof(T) == 8) {
-        s = __dmul_rn(0.25, __dadd_rn(__dadd_rn(__dadd_rn(p0[0], p0[1]), p1[0]), p1[1]));
+        s = __dmul_rn(0.25, __dadd_rn(__dadd_rn(__dadd_rn(f00, f01), f10), f11));
       } else {
-        s = __fmul_rn(0.25f, __fadd_rn(__fadd_rn(__fadd_rn(p0[0], p0[1]), p1[0]), p1[1]));
+        s = __fmul_rn(0.25f, __fadd_rn(__fadd_rn(__fadd_rn(f00, f01), f10), f11));
       }
       dec[r][c] = s;
     }
     __syncthreads();
     T* dst = out + img * (int64_t)dh * dw;
-    for (int idx = threadIdx.x; idx < kPyTile * kPyTile; idx += blockDim.x) {
-      const int r = idx / kPyTile, c = idx % kPyTile;
+    for (int idx = threadIdx.x; idx < kPyTileY * kPyTileX; idx += blockDim.x) {
+      const int r = idx / kPyTileX, c = idx - r * kPyTileX;
       const int y = ty0 + r, x = tx0 + c;
       if (y >= dh || x >= dw) continue;
       T acc = T(0);
@@ -294,15 +316,17 @@ __global__ void __launch_bounds__(256) pyramid_down_kernel(const T* __restrict__
   }
 }
 
-// ------------------------------------------------------------- host -------
-
 template <typename T>
 int launch_pyramid(const T* in, int64_t n_images, int h, int w, T* out, cudaStream_t st) {
   const int dh = h / 2, dw = w / 2;
   if (n_images == 0 || dh == 0 || dw == 0) return CT_OK;
-  const int tiles = ((dh + kPyTile - 1) / kPyTile) * ((dw + kPyTile - 1) / kPyTile);
+  const int tiles = ((dh + kPyTileY - 1) / kPyTileY) * ((dw + kPyTileX - 1) / kPyTileX);
   dim3 grid((unsigned)tiles, (unsigned)std::min<int64_t>(n_images, 65535));
-  pyramid_down_kernel<T><<<grid, 256, 0, st>>>(in, n_images, h, w, out);
+  const bool vec = (w % 2 == 0) && (reinterpret_cast<uintptr_t>(in) % (2 * sizeof(T)) == 0);
+  if (vec)
+    pyramid_down_kernel<T, true><<<grid, 256, 0, st>>>(in, n_images, h, w, out);
+  else
+    pyramid_down_kernel<T, false><<<grid, 256, 0, st>>>(in, n_images, h, w, out);
   return check_launch("pyramid_down");
 }
 
