@@ -157,9 +157,11 @@ def make_videos(V: int, seed0: int = 0):
     import paper_1612_08825_b200 as ct
     frames = torch.empty((V, NFRAMES, H, W), dtype=torch.float64, device="cuda")
     mags = [100.0 / (100.0 - t) for t in range(NFRAMES)]
-    for v in range(V):
-        tex = ct.make_texture(W, H, seed0 + v)
-        ct.zoom_frames(tex, (0.5 * W, 0.5 * H), mags, out=frames[v])
+    for v0 in range(0, V, 64):
+        seeds = list(range(seed0 + v0, seed0 + min(V, v0 + 64)))
+        tex = ct.make_textures(W, H, seeds)
+        for j in range(len(seeds)):
+            ct.zoom_frames(tex[j].contiguous(), (0.5 * W, 0.5 * H), mags, out=frames[v0 + j])
     return frames
 
 
@@ -365,9 +367,13 @@ def main():
     t_k = time_moments_kernel(frames, max(5, args.steps))
     hbm, peak_kind = load_peaks()
     achieved = V * (NFRAMES - 1) * BYTES_PER_EST / t_k / 1e9
-    traffic = load_ncu_traffic("ttc_moments_kernel<double>/cfg2")
+    tr = load_ncu_traffic("ttc_moments_kernel<double>/cfg2")
+    traffic = None
+    if tr and tr.get("videos"):
+        traffic = tr["bytes_per_launch"] * V / tr["videos"]  # scaled to this launch's video count
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-            "traffic": traffic, "kernel": "ttc_moments_kernel<double> (+ finalize)", "peak_kind": peak_kind,
+            "traffic": traffic, "traffic_unit": "bytes/launch (dram read+write, ncu --set full, profiles/)",
+            "algorithmic_bytes_per_launch": V * (NFRAMES - 1) * BYTES_PER_EST, "kernel": "ttc_moments_kernel<double> (+ finalize)", "peak_kind": peak_kind,
             "kernel_ms": t_k * 1e3, "step_ms": dt / args.steps * 1e3,
             "fp64_pipe": {"dp_ops_per_grid_px": 20, "achieved_tflops": 2 * 20 * V * (NFRAMES - 1) * 255 * 255 / t_k / 1e12 / 2,
                           "peak_tflops": 32.2, "peak_note": "DFMA-chain microbenchmark on the box (tools/fp_peak.cu)"}}

@@ -21,7 +21,7 @@ from .conv import (
     reflect,
     xcorr_direct,
 )
-from .synth import SynthConfig, approach_stream, generate, make_texture, zoom_frames
+from .synth import SynthConfig, approach_stream, generate, make_texture, make_textures, zoom_frames
 from .ttc import (
     TRACE_HEADER,
     FramePair,

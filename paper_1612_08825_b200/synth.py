@@ -76,6 +76,25 @@ def make_texture(width: int, height: int, seed: int, device="cuda") -> torch.Ten
     return (img - lo) / (hi - lo)
 
 
+def make_textures(width: int, height: int, seeds, device="cuda") -> torch.Tensor:
+    """make_texture for many seeds at once: [len(seeds), height, width] float64.
+
+    Same values as make_texture per seed (one batched conv launch per
+    smoothing pass, batched min/max), for generating benchmark inputs.
+    """
+    if width < 16 or height < 16:
+        raise ValueError(f"texture {width}x{height} too small, need >= 16")
+    noise = np.stack([np.random.Generator(np.random.PCG64(s)).random((height, width)) for s in seeds])
+    img = torch.from_numpy(noise).to(device)
+    for _ in range(2):
+        img = direct_batch(img, _B3, ConvShape.SAME, BoundaryPolicy.REPLICATE, flip=False)
+    lo = img.amin(dim=(1, 2), keepdim=True)
+    hi = img.amax(dim=(1, 2), keepdim=True)
+    flat = (hi <= lo)
+    out = (img - lo) / torch.where(flat, torch.ones_like(hi), hi - lo)
+    return torch.where(flat, torch.zeros_like(out), out)
+
+
 def zoom_frames(texture: torch.Tensor, foe_px, mags, dtype=torch.float64, out: torch.Tensor | None = None):
     """frames[t] = zoom_frame(texture, foe_px, mags[t]) on the device -> [len(mags), h, w]."""
     tex = texture.contiguous()

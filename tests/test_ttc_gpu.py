@@ -239,3 +239,12 @@ def test_full_size_batch_properties():
     # reversing time negates Et: c (and a, b) flip sign exactly
     assert np.array_equal(rev[:, 2], -fwd[:, 2])
     assert np.array_equal(rev[:, 0], -fwd[:, 0])
+
+
+def test_batched_textures_match_single():
+    seeds = [0, 5, 17]
+    batch = ct.make_textures(64, 48, seeds)
+    for j, s in enumerate(seeds):
+        assert torch.equal(batch[j], ct.make_texture(64, 48, s))
+    ref = O.make_texture(64, 48, 5)
+    assert np.array_equal(batch[1].cpu().numpy(), ref)
