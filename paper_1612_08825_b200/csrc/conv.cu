@@ -22,9 +22,14 @@
 //  * xcorr_generic<T>: any rank <= CT_MAXDIM and any kernel width; one thread
 //    per output, odometer over taps.  Used for ranks >= 4 and widths without
 //    a tiled instantiation.
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
 
 #include "common.cuh"
 
@@ -277,6 +282,201 @@ int launch_tiled(const TileArgs& a0, const T* k_host_order_taps, int ntaps, cuda
   return check_launch("xcorr_tiled");
 }
 
+// ---------------------------------------------------------------------------
+// fp32 row-pair kernel (K2/K3): packed f32x2 FMAs (FFMA2) on pairs of output
+// rows.  Output rows y and y+1 use the same tap k[j0][j1][j2] on input rows
+// y+j1 and y+1+j1, so the staged tile is kept as two row-pair interleaved
+// copies (E: rows (2p, 2p+1), O: rows (2p+1, 2p+2)); every (row r, row r+1)
+// column pair is then one aligned float2, the accumulators are (row, row+1)
+// float2 pairs, and the taps are (k, k) pairs in the parameter bank, so one
+// FFMA2 with a uniform-register tap does two output FMAs.  A thread owns
+// TZ x 2 x 8 outputs (8 consecutive columns); per (slice, tap row) it loads
+// its 8+NW-1 column window once and issues 8*NW FFMA2 per z output.
+constexpr int kPairVX = 8;
+
+struct TapsPairParam {
+  float2 v[MaxTaps<float>::value];
+};
+
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  asm volatile("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<unsigned long long*>(&c)));
+  return *reinterpret_cast<float2*>(&r);
+}
+
+// Staged pair rows insert 2 padding float2 after every 8 logical columns, so
+// thread tx's window starts at physical float2 10*tx: the eight lanes of a
+// quarter-warp then hit eight different 16-byte bank groups, and the window
+// chunk offsets 10*tx + 2c + 2*(c>>2) are compile-time per chunk.
+__host__ __device__ __forceinline__ int pair_pad(int c) { return c + ((c >> 3) << 1); }
+
+template <int NW, int TZ>
+__global__ void __launch_bounds__(256) xcorr_pair_f32(const TileArgs a, const __grid_constant__ TapsPairParam taps) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int WIN = kPairVX + NW - 1;     // window columns (float2 pairs)
+  constexpr int WLD = (WIN + 1) / 2;        // float4 loads per window
+  const int tid = threadIdx.x;
+  const int tx = tid % a.txn, ty = tid / a.txn;
+  const int BX = a.txn * kPairVX, BY = a.tyn * 2;
+  const int x0 = blockIdx.x * BX, y0 = blockIdx.y * BY;
+  const int ny = a.ny, nz = a.nz;
+  const int SY = a.sy, SXp = a.sx;          // staged rows, physical pitch (float2) of each pair copy
+  const int SXl = BX - kPairVX + 2 * WLD;   // logical staged columns (every thread's window)
+  const int PE = (SY + 1) / 2;              // pair rows in copy E
+  float2* cE = reinterpret_cast<float2*>(smem_raw);
+  float2* cO = cE + (size_t)PE * SXp;
+  const int64_t plane = (int64_t)a.my * a.mx;
+  const int64_t n_ztiles = a.batch * a.tiles_z;
+
+  for (int64_t bz = blockIdx.z; bz < n_ztiles; bz += gridDim.z) {
+    const int64_t b = bz / a.tiles_z;
+    const int z0 = (int)(bz % a.tiles_z) * TZ;
+    const float* s = reinterpret_cast<const float*>(a.s) + b * (int64_t)a.mz * plane;
+    float2 acc[TZ][kPairVX];
+#pragma unroll
+    for (int i = 0; i < TZ; ++i)
+#pragma unroll
+      for (int m = 0; m < kPairVX; ++m) acc[i][m] = make_float2(0.f, 0.f);
+
+    const int nzin = TZ + nz - 1;
+    for (int izr = 0; izr < nzin; ++izr) {
+      int gz = z0 - a.pz + izr;
+      if (gz < 0 || gz >= a.mz) {
+        if (a.boundary == CT_ZERO) continue;  // all-zero slice adds nothing
+        gz = gz < 0 ? 0 : a.mz - 1;
+      }
+      __syncthreads();
+      {
+        const float* sp = s + gz * plane;
+        const int iy0 = y0 - a.py, ix0 = x0 - a.px;
+        float* fE = reinterpret_cast<float*>(cE);
+        float* fO = reinterpret_cast<float*>(cO);
+        // one warp per staged row, lanes along the (logical) columns
+        const int lane = tid & 31, nwarps = blockDim.x >> 5;
+        for (int r = tid >> 5; r < SY; r += nwarps) {
+          int gy = iy0 + r;
+          const bool row_in = (unsigned)gy < (unsigned)a.my;
+          if (!row_in && a.boundary == CT_REPLICATE) gy = gy < 0 ? 0 : a.my - 1;
+          const float* srow = sp + (int64_t)gy * a.mx;
+          float* dE = fE + (size_t)(r >> 1) * SXp * 2 + (r & 1);
+          float* dO = r >= 1 ? fO + (size_t)((r - 1) >> 1) * SXp * 2 + ((r - 1) & 1) : nullptr;
+          for (int c = lane; c < SXl; c += 32) {
+            int gx = ix0 + c;
+            float v = 0.f;
+            if (row_in && (unsigned)gx < (unsigned)a.mx) {
+              v = __ldg(srow + gx);
+            } else if (a.boundary == CT_REPLICATE) {
+              gx = min(max(gx, 0), a.mx - 1);
+              v = __ldg(srow + gx);
+            }
+            const int cp = pair_pad(c) * 2;
+            dE[cp] = v;
+            if (dO) dO[cp] = v;
+          }
+        }
+        // the last pair row of each copy may reference a row past SY: zero it
+        if (SY & 1) {
+          for (int c = tid; c < SXp; c += blockDim.x) fE[(((SY - 1) >> 1) * SXp + c) * 2 + 1] = 0.f;
+        } else {
+          for (int c = tid; c < SXp; c += blockDim.x) fO[(((SY - 2) >> 1) * SXp + c) * 2 + 1] = 0.f;
+        }
+      }
+      __syncthreads();
+
+      for (int j1 = 0; j1 < ny; ++j1) {
+        const int lr = 2 * ty + j1;  // local input row of the pair (lr, lr+1)
+        const float2* prow = ((lr & 1) ? cO : cE) + (size_t)(lr >> 1) * SXp;
+        float2 w[2 * WLD];
+#pragma unroll
+        for (int c = 0; c < WLD; ++c) {
+          const float4 q = *reinterpret_cast<const float4*>(prow + 10 * tx + 2 * c + 2 * (c >> 2));
+          w[2 * c] = make_float2(q.x, q.y);
+          w[2 * c + 1] = make_float2(q.z, q.w);
+        }
+#pragma unroll
+        for (int zi = 0; zi < TZ; ++zi) {
+          const int j0 = izr - zi;
+          if (j0 < 0 || j0 >= nz) continue;
+          const float2* kr = taps.v + (j0 * ny + j1) * NW;
+#pragma unroll
+          for (int j2 = 0; j2 < NW; ++j2) {
+            const float2 kk = kr[j2];
+#pragma unroll
+            for (int m = 0; m < kPairVX; ++m) acc[zi][m] = ffma2(kk, w[m + j2], acc[zi][m]);
+          }
+        }
+      }
+    }
+
+    float* out = reinterpret_cast<float*>(a.out) + b * (int64_t)a.oz * a.oy * a.ox;
+#pragma unroll
+    for (int zi = 0; zi < TZ; ++zi) {
+      const int z = z0 + zi;
+      if (z >= a.oz) break;
+      const int y = y0 + 2 * ty;
+      const int x = x0 + tx * kPairVX;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (y + h >= a.oy) break;
+        float* orow = out + ((int64_t)z * a.oy + y + h) * a.ox;
+#pragma unroll
+        for (int m = 0; m < kPairVX; ++m)
+          if (x + m < a.ox) orow[x + m] = h ? acc[zi][m].y : acc[zi][m].x;
+      }
+    }
+  }
+}
+
+template <int NW, int TZ>
+int launch_pair_f32(const TileArgs& a0, const float* taps_host, int ntaps, cudaStream_t st) {
+  TileArgs a = a0;
+  TapsPairParam taps;
+  for (int i = 0; i < ntaps; ++i) taps.v[i] = make_float2(taps_host[i], taps_host[i]);
+  const int BX = a.txn * kPairVX, BY = a.tyn * 2;
+  constexpr int WIN = kPairVX + NW - 1;
+  constexpr int WLD = (WIN + 1) / 2;
+  a.sy = BY + a.ny - 1;
+  const int sxl = BX - kPairVX + 2 * WLD;  // logical columns covering every thread's window
+  a.sx = pair_pad(sxl - 1) + 1;            // physical pitch with the bank-spreading padding
+  a.sx += (a.sx & 1);                      // rows stay 16-byte aligned
+  const int PE = (a.sy + 1) / 2, PO = a.sy / 2;
+  const size_t smem = (size_t)(PE + PO) * a.sx * sizeof(float2);
+  auto kern = xcorr_pair_f32<NW, TZ>;
+  if (smem > 48 * 1024) CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 grid((unsigned)cdiv(a.ox, BX), (unsigned)cdiv(a.oy, BY),
+            (unsigned)std::min<int64_t>(a.batch * a.tiles_z, 65535));
+  kern<<<grid, a.txn * a.tyn, smem, st>>>(a, taps);
+  return check_launch("xcorr_pair_f32");
+}
+
+// Tile shape (threads along x, thread rows) minimising padded FMAs plus
+// staging over the whole output, for vx outputs per thread along x and
+// rows_per_thread output rows per thread.
+inline void choose_tile(const TileArgs& a, int nw, int vx, int rows_per_thread, int* txn, int* tyn,
+                        bool whole_warps) {
+  const double taps = (double)a.ny * (double)nw;
+  double best = 1e300;
+  for (int tx = 4; tx <= 64; ++tx) {
+    for (int ty = 1; tx * ty <= 256; ++ty) {
+      const int thr = tx * ty;
+      if (thr < 64 || (whole_warps && thr % 32 != 0)) continue;  // pair kernel stages rows per warp
+      const double bx = tx * vx, by = ty * rows_per_thread;
+      const double tiles = (double)cdiv(a.ox, (int64_t)bx) * (double)cdiv(a.oy, (int64_t)by);
+      const double warp_eff = (double)thr / (double)(cdiv(thr, 32) * 32);
+      const double stage = (bx + nw + vx) * (by + a.ny - 1);
+      const double cost = tiles * (bx * by * taps / warp_eff + 8.0 * stage);
+      if (cost < best * 0.999) {
+        best = cost;
+        *txn = tx;
+        *tyn = ty;
+      }
+    }
+  }
+}
+
 // The tiled kernel takes its taps through the kernel-parameter bank, so they
 // are needed on the host: the caller's host copy is used when given, else the
 // device kernel is copied (a few KB, synchronising the stream).  flip
@@ -292,6 +492,125 @@ int taps_to_host(const void* k, const void* k_host, int64_t n, int flip, T* dst,
   }
   for (int64_t i = 0; i < n; ++i) dst[i] = flip ? tmp[n - 1 - i] : tmp[i];
   return CT_OK;
+}
+
+// One tiled variant: kind 0 = xcorr_tiled (TY=4 rows x VX per thread),
+// kind 1 = xcorr_pair_f32 (2 rows x 8 per thread, f32 only).
+template <typename T>
+int launch_variant(TileArgs a, int kind, int nw, bool is3d, int txn, int tyn, const T* taps, int ntaps,
+                   cudaStream_t st) {
+  constexpr int VX = 16 / sizeof(T);
+  a.txn = txn;
+  a.tyn = tyn;
+  if constexpr (sizeof(T) == 4) {
+    if (kind == 1) {
+      if (is3d) {
+        a.tiles_z = (int)cdiv(a.oz, 2);
+        switch (nw) {
+#define CT_CASE(W) case W: return launch_pair_f32<W, 2>(a, reinterpret_cast<const float*>(taps), ntaps, st);
+          CT_CASE(1) CT_CASE(2) CT_CASE(3) CT_CASE(4) CT_CASE(5) CT_CASE(6) CT_CASE(7) CT_CASE(8)
+          CT_CASE(9) CT_CASE(11) CT_CASE(15) CT_CASE(31)
+#undef CT_CASE
+        }
+      } else {
+        a.tiles_z = 1;
+        switch (nw) {
+#define CT_CASE(W) case W: return launch_pair_f32<W, 1>(a, reinterpret_cast<const float*>(taps), ntaps, st);
+          CT_CASE(1) CT_CASE(2) CT_CASE(3) CT_CASE(4) CT_CASE(5) CT_CASE(6) CT_CASE(7) CT_CASE(8)
+          CT_CASE(9) CT_CASE(11) CT_CASE(15) CT_CASE(31)
+#undef CT_CASE
+        }
+      }
+      set_error("unsupported kernel width %d", nw);
+      return CT_EUNSUPPORTED;
+    }
+  }
+  if (is3d) {
+    a.tiles_z = (int)cdiv(a.oz, 2);
+    switch (nw) {
+#define CT_CASE(W) case W: return launch_tiled<T, W, VX, 4, 2>(a, taps, ntaps, st);
+      CT_CASE(1) CT_CASE(2) CT_CASE(3) CT_CASE(4) CT_CASE(5) CT_CASE(6) CT_CASE(7) CT_CASE(8)
+      CT_CASE(9) CT_CASE(11) CT_CASE(15) CT_CASE(31)
+#undef CT_CASE
+    }
+  } else {
+    a.tiles_z = 1;
+    switch (nw) {
+#define CT_CASE(W) case W: return launch_tiled<T, W, VX, 4, 1>(a, taps, ntaps, st);
+      CT_CASE(1) CT_CASE(2) CT_CASE(3) CT_CASE(4) CT_CASE(5) CT_CASE(6) CT_CASE(7) CT_CASE(8)
+      CT_CASE(9) CT_CASE(11) CT_CASE(15) CT_CASE(31)
+#undef CT_CASE
+    }
+  }
+  set_error("unsupported kernel width %d", nw);
+  return CT_EUNSUPPORTED;
+}
+
+struct Variant {
+  int kind, txn, tyn;
+};
+
+// Tile variant per problem shape, chosen once by timing a short candidate
+// list on the caller's data (the first call of a large shape synchronises
+// the stream; CT_CONV_AUTOTUNE=0 keeps the cost-model pick).
+template <typename T>
+int run_tiled_autotuned(TileArgs a, int nw, bool is3d, const T* taps, int ntaps, cudaStream_t st) {
+  constexpr int VX = 16 / sizeof(T);
+  std::vector<Variant> cands;
+  int tx = 32, ty = 8;
+  const bool f32 = sizeof(T) == 4 && getenv("CT_CONV_NOPAIR") == nullptr;
+  if (f32) {
+    choose_tile(a, nw, kPairVX, 2, &tx, &ty, true);
+    cands.push_back({1, tx, ty});
+    for (Variant v : {Variant{1, 8, 32}, Variant{1, 16, 16}, Variant{1, 16, 8}, Variant{1, 8, 16}, Variant{1, 32, 8}})
+      cands.push_back(v);
+  }
+  choose_tile(a, nw, VX, 4, &tx, &ty, false);
+  cands.push_back({0, tx, ty});
+  for (Variant v : {Variant{0, 32, 8}, Variant{0, 16, 16}, Variant{0, 32, 4}, Variant{0, 16, 8}, Variant{0, 64, 4}})
+    cands.push_back(v);
+  const double work = (double)a.batch * a.oz * a.oy * a.ox * (double)a.nz * a.ny * nw;
+  static const bool tune = !(getenv("CT_CONV_AUTOTUNE") && atoi(getenv("CT_CONV_AUTOTUNE")) == 0);
+  if (!tune || work < 2.0e8) return launch_variant<T>(a, cands[0].kind, nw, is3d, cands[0].txn, cands[0].tyn, taps, ntaps, st);
+
+  char key[256];
+  snprintf(key, sizeof(key), "%zu|%d|%d,%d,%d|%d,%d,%d|%d,%d,%d|%d,%d,%d|%d|%lld", sizeof(T), nw, a.mz, a.my, a.mx,
+           a.oz, a.oy, a.ox, a.nz, a.ny, nw, a.pz, a.py, a.px, a.boundary, (long long)a.batch);
+  static std::mutex mu;
+  static std::map<std::string, Variant> cache;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end())
+      return launch_variant<T>(a, it->second.kind, nw, is3d, it->second.txn, it->second.tyn, taps, ntaps, st);
+  }
+  cudaEvent_t e0, e1;
+  CT_CUDA(cudaEventCreate(&e0));
+  CT_CUDA(cudaEventCreate(&e1));
+  Variant best = cands[0];
+  float best_ms = 1e30f;
+  for (const Variant& v : cands) {
+    if (v.txn * v.tyn > 256 || v.txn * v.tyn < 32) continue;
+    int rc = launch_variant<T>(a, v.kind, nw, is3d, v.txn, v.tyn, taps, ntaps, st);  // warm
+    if (rc) continue;
+    CT_CUDA(cudaEventRecord(e0, st));
+    rc = launch_variant<T>(a, v.kind, nw, is3d, v.txn, v.tyn, taps, ntaps, st);
+    CT_CUDA(cudaEventRecord(e1, st));
+    CT_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (rc == CT_OK && ms < best_ms) {
+      best_ms = ms;
+      best = v;
+    }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    cache[key] = best;
+  }
+  return launch_variant<T>(a, best.kind, nw, is3d, best.txn, best.tyn, taps, ntaps, st);
 }
 
 template <typename T>
@@ -333,32 +652,9 @@ int dispatch(int ndim, const void* s, const int64_t* ms, int64_t batch, const vo
     a.pz = (int)p3[0]; a.py = (int)p3[1]; a.px = (int)p3[2];
     a.boundary = boundary;
     constexpr int VX = 16 / sizeof(T);
-    // x threads: cover the output row with as little padding as possible
-    int txn = (int)std::min<int64_t>(32, cdiv(a.ox, VX));
     const bool is3d = a.oz > 1 || a.nz > 1;
-    if (is3d) {
-      constexpr int TY = 4, TZ = 2;
-      a.txn = txn;
-      a.tyn = std::max(1, std::min<int>(256 / txn, (int)cdiv(a.oy, TY)));
-      a.tiles_z = (int)cdiv(a.oz, TZ);
-      switch (nw) {
-#define CT_CASE(W) case W: return launch_tiled<T, W, VX, TY, TZ>(a, taps_host, (int)k_elems, st);
-        CT_CASE(1) CT_CASE(2) CT_CASE(3) CT_CASE(4) CT_CASE(5) CT_CASE(6) CT_CASE(7) CT_CASE(8)
-        CT_CASE(9) CT_CASE(11) CT_CASE(15) CT_CASE(31)
-#undef CT_CASE
-      }
-    } else {
-      constexpr int TY = 4, TZ = 1;
-      a.txn = txn;
-      a.tyn = std::max(1, std::min<int>(256 / txn, (int)cdiv(a.oy, TY)));
-      a.tiles_z = 1;
-      switch (nw) {
-#define CT_CASE(W) case W: return launch_tiled<T, W, VX, TY, TZ>(a, taps_host, (int)k_elems, st);
-        CT_CASE(1) CT_CASE(2) CT_CASE(3) CT_CASE(4) CT_CASE(5) CT_CASE(6) CT_CASE(7) CT_CASE(8)
-        CT_CASE(9) CT_CASE(11) CT_CASE(15) CT_CASE(31)
-#undef CT_CASE
-      }
-    }
+    a.tiles_z = 1;
+    return run_tiled_autotuned<T>(a, nw, is3d, taps_host, (int)k_elems, st);
   }
   GenArgs g{};
   g.s = s;
