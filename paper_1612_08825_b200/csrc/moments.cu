@@ -7,8 +7,8 @@
 //   * A CTA (256 threads, one grid column each) owns a band of BR grid rows x
 //     up to 255 grid columns of one video and walks a chunk of consecutive
 //     frames.  Frame bands (BR+1 rows x 256 columns) arrive by TMA into a
-//     3-deep ring of shared-memory buffers tracked by mbarriers: while pair
-//     (t-1, t) is computed from two resident buffers, frame t+1 is in flight.
+//     ring of NB shared-memory buffers tracked by mbarriers: while pair
+//     (t-1, t) is computed from two resident buffers, frames t+1.. are in flight.
 //     Every frame is read from HBM once per band (the one-row band halo is
 //     shared with the neighbouring CTA through L2); no derivative field is
 //     ever written.
@@ -65,15 +65,16 @@ struct MomentArgs {
   int tile_cols;  // grid columns per tile
 };
 
-template <typename T, int BR>
-struct Smem {
+template <typename T, int BR, int NB>
+struct Smem {  // NB = frame-band buffers in the TMA ring (NB - 2 frames in flight per pair)
   static constexpr size_t buf_elems = (size_t)(BR + 1) * kBoxCols + 8;  // +8: masked right-neighbour reads
   static constexpr size_t buf_bytes = (buf_elems * sizeof(T) + 127) & ~size_t(127);
-  // f64 bands are large enough to host the reduction scratch in the dead
-  // buffer; f32 bands get a dedicated scratch
-  static constexpr bool red_in_buf = buf_bytes >= 10 * kThreads * sizeof(double);
-  static constexpr size_t red_bytes = red_in_buf ? 0 : 10 * kThreads * sizeof(double);
-  static constexpr size_t bars_off = 3 * buf_bytes + red_bytes;
+  // the reduction scratch lives in the dead previous-frame buffer; f32 bands
+  // are smaller, so lane pairs are combined first (half the scratch)
+  static constexpr bool half_red = buf_bytes < 10 * kThreads * sizeof(double);
+  static constexpr int red_n = half_red ? kThreads / 2 : kThreads;
+  static_assert(buf_bytes >= 10 * (size_t)red_n * sizeof(double), "reduction scratch must fit a band buffer");
+  static constexpr size_t bars_off = NB * buf_bytes;
   static constexpr size_t part_off = bars_off + 64;
   static constexpr size_t total = part_off + 10 * kRedSeg * sizeof(double);
 };
@@ -132,11 +133,11 @@ __device__ __forceinline__ void sweep(const T* __restrict__ A, const T* __restri
   m[5] = s6; m[6] = u1; m[7] = u2; m[8] = u3; m[9] = u4;
 }
 
-template <typename T, int BR>
+template <typename T, int BR, int NB>
 __global__ void __launch_bounds__(kThreads, 2) ttc_moments_kernel(const MomentArgs a,
                                                                   const __grid_constant__ CUtensorMap tmap) {
   using ACC = typename AccT<T>::type;
-  using S = Smem<T, BR>;
+  using S = Smem<T, BR, NB>;
   extern __shared__ __align__(128) unsigned char smem[];
   auto buf = [&](int k) { return reinterpret_cast<T*>(smem + (size_t)k * S::buf_bytes); };
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::bars_off);
@@ -165,13 +166,13 @@ __global__ void __launch_bounds__(kThreads, 2) ttc_moments_kernel(const MomentAr
   const int r_beg = max(1, a.border - gy0 + 1);
 
   auto issue = [&](int f) {  // frame p0+f -> buffer f%3
-    T* dst = buf(f % 3);
+    T* dst = buf(f % NB);
     const int64_t grow = row0 + (int64_t)(p0 + f) * a.h;
     if (a.use_tma) {
       if (tid == 0) {
         fence_proxy_async_smem();
-        mbar_arrive_expect_tx(&bars[f % 3], kBoxBytes);
-        tma_load_2d(dst, &tmap, &bars[f % 3], cx0, (int)grow);
+        mbar_arrive_expect_tx(&bars[f % NB], kBoxBytes);
+        tma_load_2d(dst, &tmap, &bars[f % NB], cx0, (int)grow);
       }
     } else {
       const T* src = reinterpret_cast<const T*>(a.frames) + grow * a.w;
@@ -187,11 +188,11 @@ __global__ void __launch_bounds__(kThreads, 2) ttc_moments_kernel(const MomentAr
 
   if (a.use_tma) {
     if (tid == 0) {
-      for (int i = 0; i < 3; ++i) mbar_init(&bars[i], 1);
+      for (int i = 0; i < NB; ++i) mbar_init(&bars[i], 1);
       mbar_fence_init();
     }
     __syncthreads();
-    for (int f = 0; f < min(3, nload); ++f) issue(f);
+    for (int f = 0; f < min(NB, nload); ++f) issue(f);
   } else {
     issue(0);
     issue(1);
@@ -201,11 +202,11 @@ __global__ void __launch_bounds__(kThreads, 2) ttc_moments_kernel(const MomentAr
   for (int i = 0; i < p1 - p0; ++i) {
     const int p = p0 + i;
     if (a.use_tma) {
-      mbar_wait(&bars[i % 3], (uint32_t)((i / 3) & 1));
-      mbar_wait(&bars[(i + 1) % 3], (uint32_t)(((i + 1) / 3) & 1));
+      mbar_wait(&bars[i % NB], (uint32_t)((i / NB) & 1));
+      mbar_wait(&bars[(i + 1) % NB], (uint32_t)(((i + 1) / NB) & 1));
     }
-    const T* A = buf(i % 3);
-    const T* B = buf((i + 1) % 3);
+    const T* A = buf(i % NB);
+    const T* B = buf((i + 1) % NB);
 
     ACC m[10];
     if (r_beg <= 1 && r_end >= BR)
@@ -235,25 +236,31 @@ __global__ void __launch_bounds__(kThreads, 2) ttc_moments_kernel(const MomentAr
 #pragma unroll
       for (int q = 0; q < 10; ++q) o[q] = 0.0;
     }
-    double* red = S::red_in_buf ? reinterpret_cast<double*>(const_cast<T*>(A))
-                                : reinterpret_cast<double*>(smem + 3 * S::buf_bytes);
-    __syncthreads();  // every thread is done reading A and B for this pair
+    double* red = reinterpret_cast<double*>(const_cast<T*>(A));  // frame p0+i is dead after the sweep
+    if (S::half_red) {
 #pragma unroll
-    for (int q = 0; q < 10; ++q) red[q * kThreads + tid] = o[q];
+      for (int q = 0; q < 10; ++q) o[q] += __shfl_xor_sync(0xffffffffu, o[q], 1);
+    }
+    __syncthreads();  // every thread is done reading A and B for this pair
+    if (!S::half_red || (tid & 1) == 0) {
+      const int slot = S::half_red ? tid >> 1 : tid;
+#pragma unroll
+      for (int q = 0; q < 10; ++q) red[q * S::red_n + slot] = o[q];
+    }
     __syncthreads();
-    if (tid < 10 * kRedSeg) {  // stage 1: value q, segment g sums threads g, g+16, ..., g+240
+    if (tid < 10 * kRedSeg) {  // stage 1: value q, segment g sums slots g, g+16, g+32, ...
       const int q = tid / kRedSeg, g = tid % kRedSeg;
-      const double* rq = red + q * kThreads + g;
+      const double* rq = red + q * S::red_n + g;
       double acc = 0.0;
 #pragma unroll
-      for (int j = 0; j < kThreads / kRedSeg; ++j) acc += rq[j * kRedSeg];
+      for (int j = 0; j < S::red_n / kRedSeg; ++j) acc += rq[j * kRedSeg];
       part[q * kRedSeg + g] = acc;
     }
-    __syncthreads();  // scratch consumed: buffer i%3 may be refilled
+    __syncthreads();  // scratch consumed: buffer i%NB may be refilled
     if (a.use_tma) {
-      if (i + 3 < nload) issue(i + 3);
+      if (i + NB < nload) issue(i + NB);
     } else if (i + 2 < nload) {
-      issue(i + 2);  // buffer (i+2)%3 last held frame p0+i-1
+      issue(i + 2);  // buffer (i+2)%NB last held frame p0+i+2-NB <= p0+i-1
     }
     if (tid < 10) {
       double acc = 0.0;
@@ -289,9 +296,17 @@ inline unsigned finalize_grid(int64_t n_sys) { return (unsigned)std::min<int64_t
 // Band height: 16 rows for f64 (3 x 35 KB buffers, 2 CTAs/SM, FP64-bound),
 // 32 rows for f32 (3 x 34 KB; the cheaper FP32 math needs bigger TMA
 // transfers and fewer per-pair reductions per pixel).
+// Band height: 16 rows for f64 (3 x 35 KB buffers, 2 CTAs/SM, FP64-bound),
+// 32 rows for f32 (3 x 34 KB): per-pair reduction overhead is amortised over
+// more pixels, which matters for the cheaper FP32 math (measured: 16 rows with
+// a 6-deep ring is 25% slower than 32 rows with 3 buffers).
 template <typename T>
 constexpr int band_rows() {
   return sizeof(T) == 8 ? 16 : 32;
+}
+template <typename T>
+constexpr int ring_buffers() {
+  return 3;
 }
 
 struct Plan {
@@ -356,8 +371,9 @@ int launch(const T* frames, int64_t n_videos, int n_frames, int h, int w, int bo
   static const bool no_tma = getenv("CT_NO_TMA") != nullptr;  // debugging switch: force the LDG loader
   a.use_tma = !no_tma && encode_tmap_2d(&tmap, frames, sizeof(T), (uint64_t)w,
                                         (uint64_t)(n_videos * n_frames * (int64_t)h), kBoxCols, BR + 1);
-  using S = Smem<T, BR>;
-  auto kern = ttc_moments_kernel<T, BR>;
+  constexpr int NB = ring_buffers<T>();
+  using S = Smem<T, BR, NB>;
+  auto kern = ttc_moments_kernel<T, BR, NB>;
   CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::total));
   dim3 grid((unsigned)p.units, (unsigned)p.n_chunks, (unsigned)n_videos);
   kern<<<grid, kThreads, S::total, st>>>(a, tmap);
