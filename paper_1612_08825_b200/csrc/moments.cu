@@ -63,7 +63,36 @@ struct MomentArgs {
   int chunk;      // pairs per CTA
   int use_tma;
   int tile_cols;  // grid columns per tile
+  void* dec;      // optional [n_videos][n_frames][h/2][w/2]: 2x2 block means of every frame
+  int dh, dw;
 };
+
+// The 2x2 block-mean decimation of downsample (ttc.py:202-203), written for
+// the frame resident in `buf` while it is in shared memory, so the next
+// pyramid level never re-reads the full-size frame: band rows [gy0, gy0+BR)
+// and this tile's columns map to dec rows [gy0/2, (gy0+BR)/2) and dec columns
+// [cx0/2, (cx0 + tile_cols + 1)/2), disjoint across CTAs.
+template <typename T, int BR, int NT>
+__device__ __forceinline__ void write_dec(const MomentArgs& a, const T* buf, int64_t v, int f, int gy0, int cx0,
+                                          int tid) {
+  const int dy0 = gy0 >> 1, dx0 = cx0 >> 1;
+  const int ndy = min(BR / 2, a.dh - dy0);
+  const int ndx = min((a.tile_cols + 1) >> 1, a.dw - dx0);
+  if (ndy <= 0 || ndx <= 0) return;
+  T* dst = reinterpret_cast<T*>(a.dec) + ((v * a.n_frames + f) * (int64_t)a.dh + dy0) * a.dw + dx0;
+  for (int e = tid; e < ndy * ndx; e += NT) {
+    const int yy = e / ndx, xx = e - yy * ndx;
+    const T* p0 = buf + (2 * yy) * kBoxCols + 2 * xx;
+    const T* p1 = p0 + kBoxCols;
+    T d;
+    if constexpr (sizeof(T) == 8) {
+      d = __dmul_rn(0.25, __dadd_rn(__dadd_rn(__dadd_rn(p0[0], p0[1]), p1[0]), p1[1]));
+    } else {
+      d = __fmul_rn(0.25f, __fadd_rn(__fadd_rn(__fadd_rn(p0[0], p0[1]), p1[0]), p1[1]));
+    }
+    dst[(int64_t)yy * a.dw + xx] = d;
+  }
+}
 
 template <typename T, int BR, int NB>
 struct Smem {  // NB = frame-band buffers in the TMA ring (NB - 2 frames in flight per pair)
@@ -208,6 +237,10 @@ __global__ void __launch_bounds__(kThreads, 2) ttc_moments_kernel(const MomentAr
     const T* A = buf(i % NB);
     const T* B = buf((i + 1) % NB);
 
+    if (a.dec) {  // frames p0..p1-1 belong to this chunk (the last chunk also owns frame p1)
+      write_dec<T, BR, kThreads>(a, A, v, p, gy0, cx0, tid);
+      if (p1 == n_pairs && i == p1 - p0 - 1) write_dec<T, BR, kThreads>(a, B, v, p1, gy0, cx0, tid);
+    }
     ACC m[10];
     if (r_beg <= 1 && r_end >= BR)
       sweep<T, BR, false>(A, B, tid, 1, BR, m);
@@ -344,7 +377,7 @@ size_t ws_bytes(int64_t n_videos, int n_frames, int h, int w) {
 
 template <typename T>
 int launch(const T* frames, int64_t n_videos, int n_frames, int h, int w, int border, double* sums, void* ws,
-           size_t ws_size, cudaStream_t st) {
+           size_t ws_size, void* dec, cudaStream_t st) {
   const int n_pairs = n_frames - 1;
   if (n_pairs <= 0 || n_videos == 0) return CT_OK;
   constexpr int BR = band_rows<T>();
@@ -366,6 +399,9 @@ int launch(const T* frames, int64_t n_videos, int n_frames, int h, int w, int bo
   a.units = p.units;
   a.chunk = p.chunk;
   a.tile_cols = p.tile_cols;
+  a.dec = dec;
+  a.dh = h / 2;
+  a.dw = w / 2;
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof(tmap));
   static const bool no_tma = getenv("CT_NO_TMA") != nullptr;  // debugging switch: force the LDG loader
@@ -392,10 +428,10 @@ size_t moments_workspace(int dtype, int64_t n_videos, int n_frames, int h, int w
 }
 
 int moments_launch(int dtype, const void* frames, int64_t n_videos, int n_frames, int h, int w, int border,
-                   double* sums, void* ws, size_t ws_size, cudaStream_t st) {
+                   double* sums, void* ws, size_t ws_size, cudaStream_t st, void* dec) {
   if (dtype == CT_F64)
-    return launch<double>((const double*)frames, n_videos, n_frames, h, w, border, sums, ws, ws_size, st);
-  return launch<float>((const float*)frames, n_videos, n_frames, h, w, border, sums, ws, ws_size, st);
+    return launch<double>((const double*)frames, n_videos, n_frames, h, w, border, sums, ws, ws_size, dec, st);
+  return launch<float>((const float*)frames, n_videos, n_frames, h, w, border, sums, ws, ws_size, dec, st);
 }
 
 int partials_finalize(const double* partials, int64_t n_sys, int units, double count, double* sums,

@@ -267,7 +267,10 @@ struct Vec2<float> {
 // FMA (bit-identical to the reference in float64).  A CTA stages the
 // (32+4) x (64+4) dec tile (edge-clamped) in shared memory, reading each input
 // pixel pair as one 2-element vector when the row pitch allows (VEC).
-template <typename T, bool VEC>
+// DEC=false is the blur-only stage: `in` already holds the decimated images
+// (dh x dw, written by the fused moments kernel), h x w are the undecimated
+// extents they came from.
+template <typename T, bool VEC, bool DEC = true>
 __global__ void __launch_bounds__(256) pyramid_down_kernel(const T* __restrict__ in, int64_t n_images, int h,
                                                            int w, T* __restrict__ out) {
   constexpr int SY = kPyTileY + 4, SX = kPyTileX + 4;
@@ -278,11 +281,15 @@ __global__ void __launch_bounds__(256) pyramid_down_kernel(const T* __restrict__
   const T b5[5] = {T(1.0 / 16.0), T(4.0 / 16.0), T(6.0 / 16.0), T(4.0 / 16.0), T(1.0 / 16.0)};
   using V2 = typename Vec2<T>::type;
   for (int64_t img = blockIdx.y; img < n_images; img += gridDim.y) {
-    const T* src = in + img * (int64_t)h * w;
+    const T* src = in + img * (DEC ? (int64_t)h * w : (int64_t)dh * dw);
     __syncthreads();
     for (int idx = threadIdx.x; idx < SY * SX; idx += blockDim.x) {
       const int r = idx / SX, c = idx - r * SX;
       const int yy = min(max(ty0 + r - 2, 0), dh - 1), xx = min(max(tx0 + c - 2, 0), dw - 1);
+      if (!DEC) {
+        dec[r][c] = src[(int64_t)yy * dw + xx];
+        continue;
+      }
       const T* p0 = src + (int64_t)(2 * yy) * w + 2 * xx;
       const T* p1 = p0 + w;
       T f00, f01, f10, f11;
@@ -330,6 +337,18 @@ int launch_pyramid(const T* in, int64_t n_images, int h, int w, T* out, cudaStre
   return check_launch("pyramid_down");
 }
 
+// Second half of downsample: 5x5 binomial SAME/REPLICATE over already
+// decimated images (dh x dw each, from the fused moments kernel).
+template <typename T>
+int launch_blur_dec(const T* dec, int64_t n_images, int h, int w, T* out, cudaStream_t st) {
+  const int dh = h / 2, dw = w / 2;
+  if (n_images == 0 || dh == 0 || dw == 0) return CT_OK;
+  const int tiles = ((dh + kPyTileY - 1) / kPyTileY) * ((dw + kPyTileX - 1) / kPyTileX);
+  dim3 grid((unsigned)tiles, (unsigned)std::min<int64_t>(n_images, 65535));
+  pyramid_down_kernel<T, false, false><<<grid, 256, 0, st>>>(dec, n_images, h, w, out);
+  return check_launch("pyramid_blur");
+}
+
 int launch_solve(const double* sums, int64_t count, double c_min, int level, double* est, int64_t stride,
                  cudaStream_t st) {
   if (count == 0) return CT_OK;
@@ -357,20 +376,16 @@ template <typename T>
 size_t run_seq_ws(int64_t nv, int nf, int h, int w, int level, int max_level) {
   const bool ms = max_level >= 0;
   const int nl = ms ? ms_levels(h, w, max_level) : level + 1;
-  size_t total = 0;
+  const int dt = sizeof(T) == 8 ? CT_F64 : CT_F32;
+  size_t total = 0, mom = 0;
   int lh = h, lw = w;
-  size_t mom = 0;
   for (int l = 0; l < std::max(nl, 1); ++l) {
     if (l > 0) total += align256((size_t)nv * nf * lh * lw * sizeof(T));
-    if (!ms && l != level) {
-      lh /= 2;
-      lw /= 2;
-      continue;
-    }
-    mom = std::max(mom, moments_workspace(sizeof(T) == 8 ? CT_F64 : CT_F32, nv, nf, lh, lw));
+    if (ms || l == level) mom = std::max(mom, moments_workspace(dt, nv, nf, lh, lw));
     lh /= 2;
     lw /= 2;
   }
+  if (ms && nl > 1) total += align256((size_t)nv * nf * (h / 2) * (w / 2) * sizeof(T));
   const int64_t np = nv * (nf - 1);
   total += align256(mom);
   total += align256((size_t)np * 11 * sizeof(double));
@@ -387,36 +402,40 @@ int run_seq(const T* frames, int64_t nv, int nf, int h, int w, int level, int ma
   const size_t need = run_seq_ws<T>(nv, nf, h, w, level, max_level);
   CT_REQUIRE(ws != nullptr && ws_bytes >= need, "run_sequence workspace too small (%zu < %zu)", ws_bytes, need);
   const int nl = ms ? ms_levels(h, w, max_level) : level + 1;
+  const int dt = sizeof(T) == 8 ? CT_F64 : CT_F32;
   char* cur = reinterpret_cast<char*>(ws);
-  // pyramid levels 1..nl-1
-  const T* lv = frames;
-  int lh = h, lw = w;
   const T* level_ptr[32];
   int level_h[32], level_w[32];
   level_ptr[0] = frames;
   level_h[0] = h;
   level_w[0] = w;
-  for (int l = 1; l < nl; ++l) {
-    T* dst = reinterpret_cast<T*>(cur);
-    cur += align256((size_t)nv * nf * (lh / 2) * (lw / 2) * sizeof(T));
-    int rc = launch_pyramid<T>(lv, nv * nf, lh, lw, dst, st);
-    if (rc) return rc;
-    lv = dst;
-    lh /= 2;
-    lw /= 2;
-    level_ptr[l] = dst;
-    level_h[l] = lh;
-    level_w[l] = lw;
+  T* level_buf[32] = {nullptr};
+  for (int l = 1; l < std::max(nl, 1); ++l) {  // level storage 1..nl-1
+    level_h[l] = level_h[l - 1] / 2;
+    level_w[l] = level_w[l - 1] / 2;
+    level_buf[l] = reinterpret_cast<T*>(cur);
+    level_ptr[l] = level_buf[l];
+    cur += align256((size_t)nv * nf * level_h[l] * level_w[l] * sizeof(T));
+  }
+  // the multiscale path decimates inside the moments kernel (scratch = one level-1 sized buffer)
+  T* dec_scratch = nullptr;
+  if (ms && nl > 1) {
+    dec_scratch = reinterpret_cast<T*>(cur);
+    cur += align256((size_t)nv * nf * level_h[1] * level_w[1] * sizeof(T));
   }
   size_t mom = 0;
   for (int l = 0; l < nl; ++l)
-    if (ms || l == level) mom = std::max(mom, moments_workspace(sizeof(T) == 8 ? CT_F64 : CT_F32, nv, nf, level_h[l], level_w[l]));
+    if (ms || l == level) mom = std::max(mom, moments_workspace(dt, nv, nf, level_h[l], level_w[l]));
   void* mom_ws = cur;
   cur += align256(mom);
   double* sums = reinterpret_cast<double*>(cur);
   cur += align256((size_t)np * 11 * sizeof(double));
   if (!ms) {
-    int rc = moments_launch(sizeof(T) == 8 ? CT_F64 : CT_F32, level_ptr[level], nv, nf, level_h[level], level_w[level], 1, sums, mom_ws, mom, st);
+    for (int l = 1; l <= level; ++l) {
+      int rc = launch_pyramid<T>(level_ptr[l - 1], nv * nf, level_h[l - 1], level_w[l - 1], level_buf[l], st);
+      if (rc) return rc;
+    }
+    int rc = moments_launch(dt, level_ptr[level], nv, nf, level_h[level], level_w[level], 1, sums, mom_ws, mom, st);
     if (rc) return rc;
     return launch_solve(sums, np, c_min, level, est, 10, st);
   }
@@ -426,10 +445,16 @@ int run_seq(const T* frames, int64_t nv, int nf, int h, int w, int level, int ma
   }
   double* est_levels = reinterpret_cast<double*>(cur);
   for (int l = 0; l < nl; ++l) {
-    int rc = moments_launch(sizeof(T) == 8 ? CT_F64 : CT_F32, level_ptr[l], nv, nf, level_h[l], level_w[l], 1, sums, mom_ws, mom, st);
+    const bool next = l + 1 < nl;
+    int rc = moments_launch(dt, level_ptr[l], nv, nf, level_h[l], level_w[l], 1, sums, mom_ws, mom, st,
+                            next ? dec_scratch : nullptr);
     if (rc) return rc;
     rc = launch_solve(sums, np, c_min, l, est_levels + l * 10, (int64_t)nl * 10, st);
     if (rc) return rc;
+    if (next) {
+      rc = launch_blur_dec<T>(dec_scratch, nv * nf, level_h[l], level_w[l], level_buf[l + 1], st);
+      if (rc) return rc;
+    }
   }
   multiscale_select_kernel<<<(unsigned)cdiv(np, 128), 128, 0, st>>>(est_levels, np, nl, est);
   return check_launch("multiscale_select");
