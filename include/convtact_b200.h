@@ -29,6 +29,8 @@
  *                             (ttc.py:228-305) for a stack of frames
  *   ct_zoom_frames            synth.zoom_frame / _axis_taps (synth.py:88-126), used to
  *                             generate synthetic inputs on the device
+ *   ct_gradient               kernels.gradient (kernels.py:63-72), fused SAME/REPLICATE
+ *                             pair correlation + hypot/atan2
  */
 #ifndef CONVTACT_B200_H
 #define CONVTACT_B200_H
@@ -133,6 +135,13 @@ int ct_zoom_frames(int dtype, const double* texture, int64_t h, int64_t w, doubl
                    double foe_y, const double* mags_host, int64_t n, void* frames, void* workspace,
                    size_t workspace_bytes, void* stream);
 size_t ct_zoom_frames_workspace_bytes(int64_t h, int64_t w);
+
+/* Gradient fields of `n_images` h x w images with a named kernel pair (host
+ * taps kx, ky, kh x kw <= 64): ex, ey = SAME/REPLICATE correlations, mag =
+ * hypot(ex, ey), dir = atan2(ey, ex); outputs are h x w per image. */
+int ct_gradient(int dtype, const void* img, int64_t n_images, int64_t h, int64_t w, const double* kx_host,
+                const double* ky_host, int64_t kh, int64_t kw, void* ex, void* ey, void* mag, void* dir,
+                void* stream);
 
 #ifdef __cplusplus
 }

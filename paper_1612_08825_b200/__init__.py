@@ -21,6 +21,7 @@ from .conv import (
     reflect,
     xcorr_direct,
 )
+from .kernels import KERNELS, GradientField, NamedKernel, gradient, kernel_lookup
 from .synth import SynthConfig, approach_stream, generate, make_texture, make_textures, zoom_frames
 from .ttc import (
     TRACE_HEADER,

@@ -149,8 +149,21 @@ def ttc_fixtures():
     print("ttc fixtures done")
 
 
+def gradient_fixtures():
+    from convtact.kernels import KERNELS, gradient
+    rng = np.random.default_rng(99)
+    img = rng.random((37, 53))
+    out = {"img": img}
+    for name in KERNELS:
+        f = gradient(img, name)
+        out[f"{name}_ex"], out[f"{name}_ey"], out[f"{name}_mag"], out[f"{name}_dir"] = f.ex, f.ey, f.mag, f.dir
+    np.savez_compressed(os.path.join(HERE, "gradient_fixtures.npz"), **out)
+    print("gradient fixtures done")
+
+
 if __name__ == "__main__":
     print("reference convtact", convtact.__version__)
+    gradient_fixtures()
     conv_cases()
     ttc_fixtures()
     conv_configs()

@@ -110,3 +110,20 @@ def test_fp32_rounded_multiscale_bit_exact(golden):
 def test_oracle_thread_count_invariance():
     f = O.generate(64, 64, 9, 40.0, (0.5, 0.5), 3, 0.0)
     assert np.array_equal(O.run_sequence(f, level=0, nthreads=1), O.run_sequence(f, level=0, nthreads=4))
+
+
+def test_gradient_fixtures_restated(golden):
+    # kernels.gradient (kernels.py:63-72) = SAME/REPLICATE xcorr + hypot/atan2
+    g = golden("gradient_fixtures.npz")
+    img = g["img"]
+    pairs = {"roberts": ([[1.0, 0.0], [0.0, -1.0]], [[0.0, 1.0], [-1.0, 0.0]]),
+             "prewitt2": ([[-0.5, 0.5], [-0.5, 0.5]], [[-0.5, -0.5], [0.5, 0.5]]),
+             "prewitt3": ([[-1.0, 0.0, 1.0]] * 3, [[-1.0] * 3, [0.0] * 3, [1.0] * 3]),
+             "sobel": ([[-1.0, 0.0, 1.0], [-2.0, 0.0, 2.0], [-1.0, 0.0, 1.0]],
+                       [[-1.0, -2.0, -1.0], [0.0, 0.0, 0.0], [1.0, 2.0, 1.0]])}
+    for name, (kx, ky) in pairs.items():
+        ex = O.direct(img, np.array(kx), "same", "replicate", flip=False)
+        ey = O.direct(img, np.array(ky), "same", "replicate", flip=False)
+        assert np.array_equal(ex, g[f"{name}_ex"]) and np.array_equal(ey, g[f"{name}_ey"]), name
+        assert np.array_equal(np.hypot(ex, ey), g[f"{name}_mag"]), name
+        assert np.array_equal(np.arctan2(ey, ex), g[f"{name}_dir"]), name
