@@ -283,6 +283,39 @@ __global__ void __launch_bounds__(256) pyramid_down_kernel(const T* __restrict__
   for (int64_t img = blockIdx.y; img < n_images; img += gridDim.y) {
     const T* src = in + img * (DEC ? (int64_t)h * w : (int64_t)dh * dw);
     __syncthreads();
+    if (!DEC) {  // blur-only: one warp per tile row, coalesced clamped loads, no index division
+      const int lane = threadIdx.x & 31;
+      for (int r = threadIdx.x >> 5; r < SY; r += blockDim.x >> 5) {
+        const T* srow = src + (int64_t)min(max(ty0 + r - 2, 0), dh - 1) * dw;
+#pragma unroll
+        for (int c = lane; c < SX; c += 32) dec[r][c] = srow[min(max(tx0 + c - 2, 0), dw - 1)];
+      }
+      __syncthreads();
+      // separable binomial (5 + 5 taps): this internal pyramid stage feeds the
+      // multiscale search only; the public downsample keeps the reference's
+      // 25-tap order (DEC=true path)
+      __shared__ T hrow[SY][kPyTileX + 1];
+      for (int idx = threadIdx.x; idx < SY * kPyTileX; idx += blockDim.x) {
+        const int r = idx / kPyTileX, c = idx - r * kPyTileX;
+        T acc = T(0);
+#pragma unroll
+        for (int j1 = 0; j1 < 5; ++j1) acc = fmx(b5[j1], dec[r][c + j1], acc);
+        hrow[r][c] = acc;
+      }
+      __syncthreads();
+      T* dst = out + img * (int64_t)dh * dw;
+      for (int idx = threadIdx.x; idx < kPyTileY * kPyTileX; idx += blockDim.x) {
+        const int r = idx / kPyTileX, c = idx - r * kPyTileX;
+        const int y = ty0 + r, x = tx0 + c;
+        if (y >= dh || x >= dw) continue;
+        T acc = T(0);
+#pragma unroll
+        for (int j0 = 0; j0 < 5; ++j0) acc = fmx(b5[j0], hrow[r + j0][c], acc);
+        dst[(int64_t)y * dw + x] = acc;
+      }
+      __syncthreads();  // hrow/dec reused by the next image of this CTA
+      continue;
+    }
     for (int idx = threadIdx.x; idx < SY * SX; idx += blockDim.x) {
       const int r = idx / SX, c = idx - r * SX;
       const int yy = min(max(ty0 + r - 2, 0), dh - 1), xx = min(max(tx0 + c - 2, 0), dw - 1);
