@@ -126,11 +126,14 @@ def dist_setup():
     if world > 1:
         import torch.distributed as dist
         backend = "nccl" if torch.cuda.is_available() else "gloo"
+        # CT_DIST_BACKEND=gloo exercises the multi-rank plumbing with several
+        # ranks on one GPU (host-side barriers only; kernels never wait on peers)
+        backend = os.environ.get("CT_DIST_BACKEND", backend)
         if torch.cuda.is_available():
-            torch.cuda.set_device(local)
+            torch.cuda.set_device(local % torch.cuda.device_count())
         dist.init_process_group(backend=backend)
     elif torch.cuda.is_available():
-        torch.cuda.set_device(local)
+        torch.cuda.set_device(local % torch.cuda.device_count())
     return world, rank, local
 
 
@@ -392,7 +395,8 @@ def main():
         est_h = ct.run_sequence_host(hnp, level=0)
     torch.cuda.synchronize()
     e_dt = max_over_ranks((time.perf_counter() - t0) / e_steps, world)
-    assert abs(est_h[0, 0, 5] - 97.315722253398093) <= 1e-9 * 97.3
+    if rank == 0:  # rank 0's video 0 is BASELINE config 2 itself
+        assert abs(est_h[0, 0, 5] - 97.315722253398093) <= 1e-9 * 97.3
     e2e = {"value": world * Ve * (NFRAMES - 1) / e_dt, "unit": UNIT,
            "h2d_bytes_per_step": Ve * NFRAMES * H * W * 8, "d2h_bytes_per_step": Ve * (NFRAMES - 1) * 10 * 8,
            "videos_per_step": Ve, "api": "paper_1612_08825_b200.run_sequence_host (ct_run_sequence_host)"}
