@@ -31,6 +31,8 @@
  *                             generate synthetic inputs on the device
  *   ct_gradient               kernels.gradient (kernels.py:63-72), fused SAME/REPLICATE
  *                             pair correlation + hypot/atan2
+ *   ct_decode_samples         tensor.image_read_pgm raster decode (tensor.py:104-136) on the
+ *                             device, for PGM frame ingestion
  */
 #ifndef CONVTACT_B200_H
 #define CONVTACT_B200_H
@@ -142,6 +144,11 @@ size_t ct_zoom_frames_workspace_bytes(int64_t h, int64_t w);
 int ct_gradient(int dtype, const void* img, int64_t n_images, int64_t h, int64_t w, const double* kx_host,
                 const double* ky_host, int64_t kh, int64_t kw, void* ex, void* ey, void* mag, void* dir,
                 void* stream);
+
+/* out[i] = float64(sample_i) / maxval for n raw PGM samples on the device:
+ * bytes_per_sample 1 (maxval 255) or 2 (big-endian, maxval 65535). */
+int ct_decode_samples(int bytes_per_sample, const void* raw, int64_t n, double maxval, double* out,
+                      void* stream);
 
 #ifdef __cplusplus
 }
