@@ -32,6 +32,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "tma.cuh"
 
 namespace ct {
 namespace {
@@ -262,6 +263,145 @@ __global__ void __launch_bounds__(256) xcorr_generic(const GenArgs a) {
     }
     reinterpret_cast<T*>(a.out)[i] = acc;
   }
+}
+
+// ---------------------------------------------------------------------------
+// 2-D zero-extended correlation with TMA-staged tiles (the HBM-bound small-
+// kernel case, BASELINE config 1).  Persistent CTAs walk output tiles of the
+// whole batch; each tile's input window (BY+NH-1 rows x SX columns, starting
+// at (x0-px, y0-py)) is one cp.async.bulk.tensor box whose out-of-range
+// elements the TMA unit zero-fills -- exactly the FULL/SAME zero padding, with
+// no per-element index math.  Two smem stages: the next tile streams in while
+// the current one is computed.  Compute is the xcorr_tiled register block
+// (TY rows x VX columns per thread, row-major FMA tap order: bit-identical).
+template <typename T, int NW, int VX, int TY>
+__global__ void __launch_bounds__(256) xcorr_tma2d(const TileArgs a, const __grid_constant__ TapsParam<T> taps,
+                                                   const __grid_constant__ CUtensorMap tmap) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  using V = typename VecT<T, VX>::type;
+  constexpr int CH = (VX + NW - 1 + VX - 1) / VX;
+  const int tid = threadIdx.x;
+  const int tx = tid % a.txn, ty = tid / a.txn;
+  const int BX = a.txn * VX, BY = a.tyn * TY;
+  const int tiles_x = (a.ox + BX - 1) / BX, tiles_y = (a.oy + BY - 1) / BY;
+  const int64_t n_tiles = (int64_t)tiles_x * tiles_y * a.batch;
+  const size_t stage_bytes = ((size_t)a.sx * a.sy * sizeof(T) + 127) & ~size_t(127);
+  T* stage[2] = {reinterpret_cast<T*>(smem_raw), reinterpret_cast<T*>(smem_raw + stage_bytes)};
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + 2 * stage_bytes);
+  const uint32_t box_bytes = (uint32_t)(a.sx * a.sy * sizeof(T));
+  const int ny = a.ny;
+
+  auto tile_coords = [&](int64_t t, int& x0, int& y0, int& b) {
+    b = (int)(t / ((int64_t)tiles_x * tiles_y));
+    const int r = (int)(t - (int64_t)b * tiles_x * tiles_y);
+    y0 = (r / tiles_x) * BY;
+    x0 = (r % tiles_x) * BX;
+  };
+  auto issue = [&](int64_t t, int s) {
+    int x0, y0, b;
+    tile_coords(t, x0, y0, b);
+    mbar_arrive_expect_tx(&bars[s], box_bytes);
+    tma_load_3d(stage[s], &tmap, &bars[s], x0 - a.px, y0 - a.py, b);
+  };
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  int64_t t = blockIdx.x;
+  if (tid == 0) {
+    if (t < n_tiles) issue(t, 0);
+    if (t + gridDim.x < n_tiles) issue(t + gridDim.x, 1);
+  }
+  for (int it = 0; t < n_tiles; ++it, t += gridDim.x) {
+    const int s = it & 1;
+    mbar_wait(&bars[s], (uint32_t)((it >> 1) & 1));
+    const T* tile = stage[s];
+    T acc[TY][VX];
+#pragma unroll
+    for (int j = 0; j < TY; ++j)
+#pragma unroll
+      for (int r = 0; r < VX; ++r) acc[j][r] = T(0);
+    const int nrows = TY + ny - 1;
+    for (int r = 0; r < nrows; ++r) {
+      T v[CH * VX];
+      const T* rowp = tile + (ty * TY + r) * a.sx + tx * VX;
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        const V q = *reinterpret_cast<const V*>(rowp + c * VX);
+        const T* qp = reinterpret_cast<const T*>(&q);
+#pragma unroll
+        for (int e = 0; e < VX; ++e) v[c * VX + e] = qp[e];
+      }
+#pragma unroll
+      for (int yi = 0; yi < TY; ++yi) {
+        const int j1 = r - yi;
+        if (j1 < 0 || j1 >= ny) continue;
+        const T* kr = taps.v + j1 * NW;
+#pragma unroll
+        for (int j2 = 0; j2 < NW; ++j2) {
+          const T kv = kr[j2];
+#pragma unroll
+          for (int rr = 0; rr < VX; ++rr) acc[yi][rr] = fmadd(kv, v[rr + j2], acc[yi][rr]);
+        }
+      }
+    }
+    __syncthreads();  // stage s fully read: refill it with the tile two steps ahead
+    if (tid == 0 && t + 2 * (int64_t)gridDim.x < n_tiles) {
+      fence_proxy_async_smem();
+      issue(t + 2 * (int64_t)gridDim.x, s);
+    }
+    int x0, y0, b;
+    tile_coords(t, x0, y0, b);
+    T* out = reinterpret_cast<T*>(a.out) + (int64_t)b * a.oy * a.ox;
+    const int x = x0 + tx * VX;
+    const bool vec_store = (a.ox % VX == 0) && (x + VX <= a.ox);
+#pragma unroll
+    for (int yi = 0; yi < TY; ++yi) {
+      const int y = y0 + ty * TY + yi;
+      if (y >= a.oy) break;
+      T* orow = out + (int64_t)y * a.ox;
+      if (vec_store) {
+        V q;
+        T* qp = reinterpret_cast<T*>(&q);
+#pragma unroll
+        for (int rr = 0; rr < VX; ++rr) qp[rr] = acc[yi][rr];
+        *reinterpret_cast<V*>(orow + x) = q;
+      } else {
+#pragma unroll
+        for (int rr = 0; rr < VX; ++rr)
+          if (x + rr < a.ox) orow[x + rr] = acc[yi][rr];
+      }
+    }
+  }
+}
+
+template <typename T, int NW, int VX, int TY>
+int launch_tma2d(const TileArgs& a0, const T* taps_host, int ntaps, cudaStream_t st) {
+  TileArgs a = a0;
+  TapsParam<T> taps;
+  for (int i = 0; i < ntaps; ++i) taps.v[i] = taps_host[i];
+  const int BX = a.txn * VX, BY = a.tyn * TY;
+  constexpr int CH = (VX + NW - 1 + VX - 1) / VX;
+  a.sx = BX - VX + CH * VX;
+  a.sy = BY + a.ny - 1;
+  CUtensorMap tmap;
+  memset(&tmap, 0, sizeof(tmap));
+  if (!encode_tmap_3d(&tmap, a.s, sizeof(T), (uint64_t)a.mx, (uint64_t)a.my, (uint64_t)a.batch, a.sx, a.sy)) {
+    set_error("tensor map encode failed");
+    return CT_EUNSUPPORTED;
+  }
+  const size_t stage_bytes = ((size_t)a.sx * a.sy * sizeof(T) + 127) & ~size_t(127);
+  const size_t smem = 2 * stage_bytes + 16;
+  auto kern = xcorr_tma2d<T, NW, VX, TY>;
+  CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  CT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, a.txn * a.tyn, smem));
+  const int64_t tiles = cdiv(a.ox, BX) * cdiv(a.oy, BY) * a.batch;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)num_sms() * std::max(1, per_sm)));
+  kern<<<grid, a.txn * a.tyn, smem, st>>>(a, taps, tmap);
+  return check_launch("xcorr_tma2d");
 }
 
 template <typename T, int NW, int VX, int TY, int TZ>
@@ -525,6 +665,17 @@ int launch_variant(TileArgs a, int kind, int nw, bool is3d, int txn, int tyn, co
       return CT_EUNSUPPORTED;
     }
   }
+  if (kind == 2) {  // TMA-staged persistent 2-D kernel (zero boundary, aligned; see tma_ok)
+    a.tiles_z = 1;
+    switch (nw) {
+#define CT_CASE(W) case W: return launch_tma2d<T, W, VX, 4>(a, taps, ntaps, st);
+      CT_CASE(1) CT_CASE(2) CT_CASE(3) CT_CASE(4) CT_CASE(5) CT_CASE(6) CT_CASE(7) CT_CASE(8)
+      CT_CASE(9) CT_CASE(11) CT_CASE(15) CT_CASE(31)
+#undef CT_CASE
+    }
+    set_error("unsupported kernel width %d", nw);
+    return CT_EUNSUPPORTED;
+  }
   if (is3d) {
     a.tiles_z = (int)cdiv(a.oz, 2);
     switch (nw) {
@@ -569,8 +720,23 @@ int run_tiled_autotuned(TileArgs a, int nw, bool is3d, const T* taps, int ntaps,
   cands.push_back({0, tx, ty});
   for (Variant v : {Variant{0, 32, 8}, Variant{0, 16, 16}, Variant{0, 32, 4}, Variant{0, 16, 8}, Variant{0, 64, 4}})
     cands.push_back(v);
+  // TMA staging: 2-D, zero extension, box start and row pitch 16-byte aligned
+  const bool tma_ok = !is3d && a.boundary == CT_ZERO && (a.px * (int)sizeof(T)) % 16 == 0 &&
+                      (a.mx * (int64_t)sizeof(T)) % 16 == 0 && (reinterpret_cast<uintptr_t>(a.s) & 15) == 0 &&
+                      getenv("CT_CONV_NOTMA") == nullptr;
+  if (tma_ok) {
+    for (Variant v : {Variant{2, 32, 8}, Variant{2, 16, 16}, Variant{2, 32, 4}, Variant{2, 16, 8}, Variant{2, 64, 4}}) {
+      const int sx = v.txn * VX - VX + (int)cdiv(VX + nw - 1, VX) * VX, sy = v.tyn * 4 + a.ny - 1;
+      if (sx <= 256 && sy <= 256) cands.push_back(v);
+    }
+  }
   const double work = (double)a.batch * a.oz * a.oy * a.ox * (double)a.nz * a.ny * nw;
   static const bool tune = !(getenv("CT_CONV_AUTOTUNE") && atoi(getenv("CT_CONV_AUTOTUNE")) == 0);
+  if (const char* force = getenv("CT_CONV_KIND")) {  // tests: pin one variant family
+    const int kind = atoi(force);
+    for (const Variant& v : cands)
+      if (v.kind == kind) return launch_variant<T>(a, v.kind, nw, is3d, v.txn, v.tyn, taps, ntaps, st);
+  }
   if (!tune || work < 2.0e8) return launch_variant<T>(a, cands[0].kind, nw, is3d, cands[0].txn, cands[0].tyn, taps, ntaps, st);
 
   char key[256];

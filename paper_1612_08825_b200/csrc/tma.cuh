@@ -52,6 +52,20 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y,
+                                            int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Rank-3 tiled map over [d2][d1][d0] elements (d0 contiguous) with a box of
+// box0 x box1 x 1; out-of-range reads are zero-filled.
+bool encode_tmap_3d(CUtensorMap* map, const void* base, int esz, uint64_t d0, uint64_t d1, uint64_t d2,
+                    uint32_t box0, uint32_t box1);
+
 // Encode a rank-2 tiled tensor map over a row-major [rows][cols] array of
 // `esz`-byte elements with a box of box_cols x box_rows; out-of-range reads
 // are zero-filled.  Returns false if the layout is not TMA-compatible
