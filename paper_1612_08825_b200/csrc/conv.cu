@@ -274,11 +274,17 @@ __global__ void __launch_bounds__(256) xcorr_generic(const GenArgs a) {
 // no per-element index math.  Two smem stages: the next tile streams in while
 // the current one is computed.  Compute is the xcorr_tiled register block
 // (TY rows x VX columns per thread, row-major FMA tap order: bit-identical).
-template <typename T, int NW, int VX, int TY>
+// outputs per thread along x in the TMA kernel: one 16-byte vector (measured:
+// 4 doubles per thread is 20% slower than 2 on config 1)
+template <typename T>
+constexpr int tma_vx() { return 16 / sizeof(T); }
+
+template <typename T, int NW, int VX, int TY, int NH>
 __global__ void __launch_bounds__(256) xcorr_tma2d(const TileArgs a, const __grid_constant__ TapsParam<T> taps,
                                                    const __grid_constant__ CUtensorMap tmap) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  using V = typename VecT<T, VX>::type;
+  constexpr int VW = 16 / sizeof(T);  // elements per 16-byte vector; VX is a multiple of it
+  using V = typename VecT<T, VW>::type;
   constexpr int CH = (VX + NW - 1 + VX - 1) / VX;
   const int tid = threadIdx.x;
   const int tx = tid % a.txn, ty = tid / a.txn;
@@ -286,7 +292,7 @@ __global__ void __launch_bounds__(256) xcorr_tma2d(const TileArgs a, const __gri
   const int tiles_x = (a.ox + BX - 1) / BX, tiles_y = (a.oy + BY - 1) / BY;
   const int64_t n_tiles = (int64_t)tiles_x * tiles_y * a.batch;
   const size_t stage_bytes = ((size_t)a.sx * a.sy * sizeof(T) + 127) & ~size_t(127);
-  T* stage[2] = {reinterpret_cast<T*>(smem_raw), reinterpret_cast<T*>(smem_raw + stage_bytes)};
+  auto stage = [&](int s) { return reinterpret_cast<T*>(smem_raw + (size_t)s * stage_bytes); };
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + 2 * stage_bytes);
   const uint32_t box_bytes = (uint32_t)(a.sx * a.sy * sizeof(T));
   const int ny = a.ny;
@@ -301,7 +307,7 @@ __global__ void __launch_bounds__(256) xcorr_tma2d(const TileArgs a, const __gri
     int x0, y0, b;
     tile_coords(t, x0, y0, b);
     mbar_arrive_expect_tx(&bars[s], box_bytes);
-    tma_load_3d(stage[s], &tmap, &bars[s], x0 - a.px, y0 - a.py, b);
+    tma_load_3d(stage(s), &tmap, &bars[s], x0 - a.px, y0 - a.py, b);
   };
   if (tid == 0) {
     mbar_init(&bars[0], 1);
@@ -317,27 +323,32 @@ __global__ void __launch_bounds__(256) xcorr_tma2d(const TileArgs a, const __gri
   for (int it = 0; t < n_tiles; ++it, t += gridDim.x) {
     const int s = it & 1;
     mbar_wait(&bars[s], (uint32_t)((it >> 1) & 1));
-    const T* tile = stage[s];
+    const T* tile = stage(s);
     T acc[TY][VX];
 #pragma unroll
     for (int j = 0; j < TY; ++j)
 #pragma unroll
       for (int r = 0; r < VX; ++r) acc[j][r] = T(0);
-    const int nrows = TY + ny - 1;
-    for (int r = 0; r < nrows; ++r) {
+    // NH > 0: kernel height known at compile time -> the row loop unrolls and
+    // every tap index is a constant (taps become constant-bank operands)
+    const int nrows = TY + (NH > 0 ? NH : ny) - 1;
+#pragma unroll
+    for (int r = 0; r < (NH > 0 ? TY + NH - 1 : nrows); ++r) {
       T v[CH * VX];
       const T* rowp = tile + (ty * TY + r) * a.sx + tx * VX;
 #pragma unroll
-      for (int c = 0; c < CH; ++c) {
-        const V q = *reinterpret_cast<const V*>(rowp + c * VX);
-        const T* qp = reinterpret_cast<const T*>(&q);
+      for (int c = 0; c < CH; ++c)
 #pragma unroll
-        for (int e = 0; e < VX; ++e) v[c * VX + e] = qp[e];
-      }
+        for (int k = 0; k < VX / VW; ++k) {
+          const V q = *reinterpret_cast<const V*>(rowp + c * VX + k * VW);
+          const T* qp = reinterpret_cast<const T*>(&q);
+#pragma unroll
+          for (int e = 0; e < VW; ++e) v[c * VX + k * VW + e] = qp[e];
+        }
 #pragma unroll
       for (int yi = 0; yi < TY; ++yi) {
         const int j1 = r - yi;
-        if (j1 < 0 || j1 >= ny) continue;
+        if (j1 < 0 || j1 >= (NH > 0 ? NH : ny)) continue;
         const T* kr = taps.v + j1 * NW;
 #pragma unroll
         for (int j2 = 0; j2 < NW; ++j2) {
@@ -356,18 +367,21 @@ __global__ void __launch_bounds__(256) xcorr_tma2d(const TileArgs a, const __gri
     tile_coords(t, x0, y0, b);
     T* out = reinterpret_cast<T*>(a.out) + (int64_t)b * a.oy * a.ox;
     const int x = x0 + tx * VX;
-    const bool vec_store = (a.ox % VX == 0) && (x + VX <= a.ox);
+    const bool vec_store = (a.ox % VW == 0) && (x + VX <= a.ox);
 #pragma unroll
     for (int yi = 0; yi < TY; ++yi) {
       const int y = y0 + ty * TY + yi;
       if (y >= a.oy) break;
       T* orow = out + (int64_t)y * a.ox;
       if (vec_store) {
-        V q;
-        T* qp = reinterpret_cast<T*>(&q);
 #pragma unroll
-        for (int rr = 0; rr < VX; ++rr) qp[rr] = acc[yi][rr];
-        *reinterpret_cast<V*>(orow + x) = q;
+        for (int k = 0; k < VX / VW; ++k) {
+          V q;
+          T* qp = reinterpret_cast<T*>(&q);
+#pragma unroll
+          for (int e = 0; e < VW; ++e) qp[e] = acc[yi][k * VW + e];
+          *reinterpret_cast<V*>(orow + x + k * VW) = q;
+        }
       } else {
 #pragma unroll
         for (int rr = 0; rr < VX; ++rr)
@@ -377,7 +391,7 @@ __global__ void __launch_bounds__(256) xcorr_tma2d(const TileArgs a, const __gri
   }
 }
 
-template <typename T, int NW, int VX, int TY>
+template <typename T, int NW, int VX, int TY, int NH>
 int launch_tma2d(const TileArgs& a0, const T* taps_host, int ntaps, cudaStream_t st) {
   TileArgs a = a0;
   TapsParam<T> taps;
@@ -394,7 +408,7 @@ int launch_tma2d(const TileArgs& a0, const T* taps_host, int ntaps, cudaStream_t
   }
   const size_t stage_bytes = ((size_t)a.sx * a.sy * sizeof(T) + 127) & ~size_t(127);
   const size_t smem = 2 * stage_bytes + 16;
-  auto kern = xcorr_tma2d<T, NW, VX, TY>;
+  auto kern = xcorr_tma2d<T, NW, VX, TY, NH>;
   CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   CT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, a.txn * a.tyn, smem));
@@ -668,7 +682,10 @@ int launch_variant(TileArgs a, int kind, int nw, bool is3d, int txn, int tyn, co
   if (kind == 2) {  // TMA-staged persistent 2-D kernel (zero boundary, aligned; see tma_ok)
     a.tiles_z = 1;
     switch (nw) {
-#define CT_CASE(W) case W: return launch_tma2d<T, W, VX, 4>(a, taps, ntaps, st);
+#define CT_CASE(W)                                                                          \
+  case W:                                                                                   \
+    if (a.ny == W && (W == 3 || W == 5 || W == 7)) return launch_tma2d<T, W, tma_vx<T>(), 4, W>(a, taps, ntaps, st); \
+    return launch_tma2d<T, W, tma_vx<T>(), 4, 0>(a, taps, ntaps, st);
       CT_CASE(1) CT_CASE(2) CT_CASE(3) CT_CASE(4) CT_CASE(5) CT_CASE(6) CT_CASE(7) CT_CASE(8)
       CT_CASE(9) CT_CASE(11) CT_CASE(15) CT_CASE(31)
 #undef CT_CASE
@@ -726,7 +743,8 @@ int run_tiled_autotuned(TileArgs a, int nw, bool is3d, const T* taps, int ntaps,
                       getenv("CT_CONV_NOTMA") == nullptr;
   if (tma_ok) {
     for (Variant v : {Variant{2, 32, 8}, Variant{2, 16, 16}, Variant{2, 32, 4}, Variant{2, 16, 8}, Variant{2, 64, 4}}) {
-      const int sx = v.txn * VX - VX + (int)cdiv(VX + nw - 1, VX) * VX, sy = v.tyn * 4 + a.ny - 1;
+      constexpr int tv = tma_vx<T>();
+      const int sx = v.txn * tv - tv + (int)cdiv(tv + nw - 1, tv) * tv, sy = v.tyn * 4 + a.ny - 1;
       if (sx <= 256 && sy <= 256) cands.push_back(v);
     }
   }
