@@ -29,6 +29,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -282,7 +283,7 @@ constexpr int tma_vx() { return 16 / sizeof(T); }
 template <typename T, int NW, int VX, int TY, int NH>
 __global__ void __launch_bounds__(256) xcorr_tma2d(const TileArgs a, const __grid_constant__ TapsParam<T> taps,
                                                    const __grid_constant__ CUtensorMap tmap) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_tma[];
   constexpr int VW = 16 / sizeof(T);  // elements per 16-byte vector; VX is a multiple of it
   using V = typename VecT<T, VW>::type;
   constexpr int CH = (VX + NW - 1 + VX - 1) / VX;
@@ -292,8 +293,8 @@ __global__ void __launch_bounds__(256) xcorr_tma2d(const TileArgs a, const __gri
   const int tiles_x = (a.ox + BX - 1) / BX, tiles_y = (a.oy + BY - 1) / BY;
   const int64_t n_tiles = (int64_t)tiles_x * tiles_y * a.batch;
   const size_t stage_bytes = ((size_t)a.sx * a.sy * sizeof(T) + 127) & ~size_t(127);
-  auto stage = [&](int s) { return reinterpret_cast<T*>(smem_raw + (size_t)s * stage_bytes); };
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + 2 * stage_bytes);
+  auto stage = [&](int s) { return reinterpret_cast<T*>(smem_tma + (size_t)s * stage_bytes); };
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_tma + 2 * stage_bytes);
   const uint32_t box_bytes = (uint32_t)(a.sx * a.sy * sizeof(T));
   const int ny = a.ny;
 
@@ -416,6 +417,185 @@ int launch_tma2d(const TileArgs& a0, const T* taps_host, int ntaps, cudaStream_t
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)num_sms() * std::max(1, per_sm)));
   kern<<<grid, a.txn * a.tyn, smem, st>>>(a, taps, tmap);
   return check_launch("xcorr_tma2d");
+}
+
+template <typename T, int LW>
+struct LoadT;
+template <>
+struct LoadT<float, 4> {
+  using type = float4;
+};
+template <>
+struct LoadT<float, 2> {
+  using type = float2;
+};
+template <>
+struct LoadT<float, 1> {
+  using type = float;
+};
+template <>
+struct LoadT<double, 2> {
+  using type = double2;
+};
+template <>
+struct LoadT<double, 1> {
+  using type = double;
+};
+
+// ---------------------------------------------------------------------------
+// 3-D zero-extended correlation with TMA-staged z-slices (BASELINE config 3).
+// A CTA owns TZ output slices x (BY x BX) of one volume and walks the input
+// slices that feed them through a 2-stage TMA ring (4-D tensor map
+// {x, y, z, batch}: out-of-range slices, rows and columns arrive as zeros).
+// The box starts at x0 - pxa with pxa = px rounded up to a 16-byte multiple,
+// so the window of thread tx begins `sh` = pxa - px elements into its staged
+// row; LW (elements per shared load: 4, 2 or 1) keeps those loads aligned.
+template <typename T, int NW, int VX, int TY, int TZ, int LW>
+__global__ void __launch_bounds__(256) xcorr_tma3d(const TileArgs a, const __grid_constant__ TapsParam<T> taps,
+                                                   const __grid_constant__ CUtensorMap tmap, int pxa) {
+  extern __shared__ __align__(128) unsigned char smem_tma[];
+  constexpr int CHL = (VX + NW - 1 + LW - 1) / LW;  // window loads per row
+  using L = typename LoadT<T, LW>::type;
+  const int tid = threadIdx.x;
+  const int tx = tid % a.txn, ty = tid / a.txn;
+  const int BX = a.txn * VX, BY = a.tyn * TY;
+  const int x0 = blockIdx.x * BX, y0 = blockIdx.y * BY;
+  const int sh = pxa - a.px;
+  const size_t stage_bytes = ((size_t)a.sx * a.sy * sizeof(T) + 127) & ~size_t(127);
+  auto stage = [&](int s) { return reinterpret_cast<T*>(smem_tma + (size_t)s * stage_bytes); };
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_tma + 2 * stage_bytes);
+  const uint32_t box_bytes = (uint32_t)(a.sx * a.sy * sizeof(T));
+  const int ny = a.ny, nz = a.nz;
+  const int64_t n_ztiles = a.batch * a.tiles_z;
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  int gcount = 0;  // slices this CTA has consumed so far: stage = g & 1, phase = (g >> 1) & 1
+  for (int64_t bz = blockIdx.z; bz < n_ztiles; bz += gridDim.z) {
+    const int b = (int)(bz / a.tiles_z);
+    const int z0 = (int)(bz % a.tiles_z) * TZ;
+    // input slices gz in [z0 - pz, z0 - pz + TZ + nz - 1) that exist
+    const int g_lo = max(0, z0 - a.pz), g_hi = min(a.mz, z0 - a.pz + TZ + nz - 1);
+    const int nsl = max(0, g_hi - g_lo);
+    const int g0 = gcount;
+    auto issue = [&](int k) {  // k-th existing slice -> stage (g0 + k) & 1
+      if (tid == 0) {
+        const int sg = (g0 + k) & 1;
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&bars[sg], box_bytes);
+        tma_load_4d(stage(sg), &tmap, &bars[sg], x0 - pxa, y0 - a.py, g_lo + k, b);
+      }
+    };
+    if (nsl > 0) issue(0);
+    if (nsl > 1) issue(1);
+    T acc[TZ][TY][VX];
+#pragma unroll
+    for (int i = 0; i < TZ; ++i)
+#pragma unroll
+      for (int j = 0; j < TY; ++j)
+#pragma unroll
+        for (int r = 0; r < VX; ++r) acc[i][j][r] = T(0);
+    for (int k = 0; k < nsl; ++k) {
+      const int g = g0 + k;
+      const int s = g & 1;
+      mbar_wait(&bars[s], (uint32_t)((g >> 1) & 1));
+      const T* tile = stage(s);
+      const int izr = g_lo + k - (z0 - a.pz);  // slice index relative to the window start
+      const int nrows = TY + ny - 1;
+      for (int r = 0; r < nrows; ++r) {
+        T v[CHL * LW];
+        const T* rowp = tile + (ty * TY + r) * a.sx + sh + tx * VX;
+#pragma unroll
+        for (int c = 0; c < CHL; ++c) {
+          const L q = *reinterpret_cast<const L*>(rowp + c * LW);
+          const T* qp = reinterpret_cast<const T*>(&q);
+#pragma unroll
+          for (int e = 0; e < LW; ++e) v[c * LW + e] = qp[e];
+        }
+#pragma unroll
+        for (int zi = 0; zi < TZ; ++zi) {
+          const int j0 = izr - zi;
+          if (j0 < 0 || j0 >= nz) continue;
+#pragma unroll
+          for (int yi = 0; yi < TY; ++yi) {
+            const int j1 = r - yi;
+            if (j1 < 0 || j1 >= ny) continue;
+            const T* kr = taps.v + (j0 * ny + j1) * NW;
+#pragma unroll
+            for (int j2 = 0; j2 < NW; ++j2) {
+              const T kv = kr[j2];
+#pragma unroll
+              for (int rr = 0; rr < VX; ++rr) acc[zi][yi][rr] = fmadd(kv, v[rr + j2], acc[zi][yi][rr]);
+            }
+          }
+        }
+      }
+      __syncthreads();  // stage s consumed
+      if (k + 2 < nsl) issue(k + 2);
+    }
+    gcount += nsl;
+    T* out = reinterpret_cast<T*>(a.out) + (int64_t)b * a.oz * a.oy * a.ox;
+#pragma unroll
+    for (int zi = 0; zi < TZ; ++zi) {
+      const int z = z0 + zi;
+      if (z >= a.oz) break;
+#pragma unroll
+      for (int yi = 0; yi < TY; ++yi) {
+        const int y = y0 + ty * TY + yi;
+        if (y >= a.oy) break;
+        T* orow = out + ((int64_t)z * a.oy + y) * a.ox;
+        const int x = x0 + tx * VX;
+#pragma unroll
+        for (int rr = 0; rr < VX; ++rr)
+          if (x + rr < a.ox) orow[x + rr] = acc[zi][yi][rr];
+      }
+    }
+  }
+}
+
+template <typename T, int NW, int VX, int TY, int TZ>
+int launch_tma3d(const TileArgs& a0, const T* taps_host, int ntaps, cudaStream_t st) {
+  TileArgs a = a0;
+  TapsParam<T> taps;
+  for (int i = 0; i < ntaps; ++i) taps.v[i] = taps_host[i];
+  constexpr int VW = 16 / sizeof(T);
+  const int pxa = (a.px + VW - 1) / VW * VW;
+  const int sh = pxa - a.px;
+  const int BX = a.txn * VX, BY = a.tyn * TY;
+  a.sx = sh + BX + NW - 1;
+  a.sx = (a.sx + VW - 1) / VW * VW;  // 16-byte box rows
+  a.sy = BY + a.ny - 1;
+  a.tiles_z = (int)cdiv(a.oz, TZ);
+  CUtensorMap tmap;
+  memset(&tmap, 0, sizeof(tmap));
+  if (!encode_tmap_4d(&tmap, a.s, sizeof(T), (uint64_t)a.mx, (uint64_t)a.my, (uint64_t)a.mz, (uint64_t)a.batch, a.sx,
+                      a.sy)) {
+    set_error("tensor map encode failed");
+    return CT_EUNSUPPORTED;
+  }
+  const size_t stage_bytes = ((size_t)a.sx * a.sy * sizeof(T) + 127) & ~size_t(127);
+  const size_t smem = 2 * stage_bytes + 16 + 16;  // + barriers; window over-read of <= 12 bytes stays inside
+  dim3 grid((unsigned)cdiv(a.ox, BX), (unsigned)cdiv(a.oy, BY),
+            (unsigned)std::min<int64_t>(a.batch * a.tiles_z, 65535));
+  int rc;
+  if (sh % 4 == 0 && VW == 4) {
+    auto kern = xcorr_tma3d<T, NW, VX, TY, TZ, (VW == 4 ? 4 : 2)>;
+    CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<grid, a.txn * a.tyn, smem, st>>>(a, taps, tmap, pxa);
+  } else if (sh % 2 == 0) {
+    auto kern = xcorr_tma3d<T, NW, VX, TY, TZ, 2>;
+    CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<grid, a.txn * a.tyn, smem, st>>>(a, taps, tmap, pxa);
+  } else {
+    auto kern = xcorr_tma3d<T, NW, VX, TY, TZ, 1>;
+    CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<grid, a.txn * a.tyn, smem, st>>>(a, taps, tmap, pxa);
+  }
+  rc = check_launch("xcorr_tma3d");
+  return rc;
 }
 
 template <typename T, int NW, int VX, int TY, int TZ>
@@ -693,6 +873,16 @@ int launch_variant(TileArgs a, int kind, int nw, bool is3d, int txn, int tyn, co
     set_error("unsupported kernel width %d", nw);
     return CT_EUNSUPPORTED;
   }
+  if (kind == 3) {  // TMA-staged 3-D kernel (zero boundary, aligned rows; see tma3_ok)
+    switch (nw) {
+#define CT_CASE(W) case W: return launch_tma3d<T, W, VX, 4, 2>(a, taps, ntaps, st);
+      CT_CASE(1) CT_CASE(2) CT_CASE(3) CT_CASE(4) CT_CASE(5) CT_CASE(6) CT_CASE(7) CT_CASE(8)
+      CT_CASE(9) CT_CASE(11) CT_CASE(15) CT_CASE(31)
+#undef CT_CASE
+    }
+    set_error("unsupported kernel width %d", nw);
+    return CT_EUNSUPPORTED;
+  }
   if (is3d) {
     a.tiles_z = (int)cdiv(a.oz, 2);
     switch (nw) {
@@ -746,6 +936,17 @@ int run_tiled_autotuned(TileArgs a, int nw, bool is3d, const T* taps, int ntaps,
       constexpr int tv = tma_vx<T>();
       const int sx = v.txn * tv - tv + (int)cdiv(tv + nw - 1, tv) * tv, sy = v.tyn * 4 + a.ny - 1;
       if (sx <= 256 && sy <= 256) cands.push_back(v);
+    }
+  }
+  // 3-D TMA staging: zero extension, 16-byte row pitch and base (any px)
+  const bool tma3_ok = is3d && a.boundary == CT_ZERO && (a.mx * (int64_t)sizeof(T)) % 16 == 0 &&
+                       (reinterpret_cast<uintptr_t>(a.s) & 15) == 0 && a.batch < (1ll << 31) &&
+                       getenv("CT_CONV_NOTMA") == nullptr;
+  if (tma3_ok) {
+    for (Variant v : {Variant{3, 32, 8}, Variant{3, 16, 16}, Variant{3, 32, 4}, Variant{3, 16, 8}, Variant{3, 8, 16}}) {
+      constexpr int vw = 16 / (int)sizeof(T);
+      const int sx = (vw + v.txn * VX + nw - 1 + vw - 1) / vw * vw, sy = v.tyn * 4 + a.ny - 1;
+      if (sx <= 256 && sy <= 256 && 2 * (size_t)sx * sy * sizeof(T) + 512 <= 227 * 1024) cands.push_back(v);
     }
   }
   const double work = (double)a.batch * a.oz * a.oy * a.ox * (double)a.nz * a.ny * nw;
@@ -835,7 +1036,6 @@ int dispatch(int ndim, const void* s, const int64_t* ms, int64_t batch, const vo
     a.nz = (int)n3[0]; a.ny = (int)n3[1];
     a.pz = (int)p3[0]; a.py = (int)p3[1]; a.px = (int)p3[2];
     a.boundary = boundary;
-    constexpr int VX = 16 / sizeof(T);
     const bool is3d = a.oz > 1 || a.nz > 1;
     a.tiles_z = 1;
     return run_tiled_autotuned<T>(a, nw, is3d, taps_host, (int)k_elems, st);

@@ -59,4 +59,21 @@ bool encode_tmap_3d(CUtensorMap* map, const void* base, int esz, uint64_t d0, ui
   return r == CUDA_SUCCESS;
 }
 
+bool encode_tmap_4d(CUtensorMap* map, const void* base, int esz, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t d3,
+                    uint32_t box0, uint32_t box1) {
+  if ((reinterpret_cast<uintptr_t>(base) & 15) != 0) return false;
+  if ((d0 * esz) % 16 != 0 || (box0 * esz) % 16 != 0 || box0 > 256 || box1 > 256) return false;
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[4] = {d0, d1, d2, d3};
+  cuuint64_t strides[3] = {d0 * (cuuint64_t)esz, d0 * d1 * (cuuint64_t)esz, d0 * d1 * d2 * (cuuint64_t)esz};
+  cuuint32_t box[4] = {box0, box1, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(map, esz == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+                  const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 }  // namespace ct

@@ -61,6 +61,19 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y,
+                                            int z, int w) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(w), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Rank-4 tiled map over [d3][d2][d1][d0] elements with a box0 x box1 x 1 x 1 box.
+bool encode_tmap_4d(CUtensorMap* map, const void* base, int esz, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t d3,
+                    uint32_t box0, uint32_t box1);
+
 // Rank-3 tiled map over [d2][d1][d0] elements (d0 contiguous) with a box of
 // box0 x box1 x 1; out-of-range reads are zero-filled.
 bool encode_tmap_3d(CUtensorMap* map, const void* base, int esz, uint64_t d0, uint64_t d1, uint64_t d2,

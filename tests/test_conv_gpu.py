@@ -224,3 +224,25 @@ def test_each_kernel_variant_matches_oracle(kind, monkeypatch):
         for i in range(3):
             ref = O.direct(s32[i].astype(np.float64), k32.astype(np.float64), shape.value, "zero", True)
             assert rel_inf(g32[i], ref) <= 1e-5, (kind, ms, ns)
+
+
+@pytest.mark.parametrize("kind", ["0", "1", "3"])
+def test_each_3d_kernel_variant_matches_oracle(kind, monkeypatch):
+    """3-D shapes with each tiled variant pinned (3 = TMA-staged z-slices, used for
+    zero extension with 16-byte rows; odd rows fall back): fp64 bit-exact, fp32 1e-5."""
+    monkeypatch.setenv("CT_CONV_KIND", kind)
+    rng = np.random.default_rng(int(kind) + 70)
+    for ms, ns, shape in [((20, 33, 64), (5, 5, 5), F), ((17, 40, 36), (3, 3, 3), S),
+                          ((9, 24, 32), (3, 5, 7), V), ((12, 30, 41), (3, 3, 5), F),
+                          ((6, 70, 300), (2, 4, 9), S)]:
+        s64 = rng.random((2,) + ms)
+        k64 = rng.standard_normal(ns)
+        got = ct.direct_batch(torch.from_numpy(s64).cuda(), k64, shape, flip=False).cpu().numpy()
+        for i in range(2):
+            assert np.array_equal(got[i], O.direct(s64[i], k64, shape.value, "zero", False)), (kind, ms, ns)
+        s32 = s64.astype(np.float32)
+        k32 = k64.astype(np.float32)
+        g32 = ct.direct_batch(torch.from_numpy(s32).cuda(), k32, shape, flip=False).cpu().numpy()
+        for i in range(2):
+            ref = O.direct(s32[i].astype(np.float64), k32.astype(np.float64), shape.value, "zero", False)
+            assert rel_inf(g32[i], ref) <= 1e-5, (kind, ms, ns)
