@@ -21,7 +21,7 @@
 //     Et^2} and U = {Ex H, Ey H, H Et, H H}; then sum(Ex G) = xc S1 + U1,
 //     sum(Ey G) = xc S2 + U2, sum(G Et) = xc S4 + U3, sum(G^2) = xc^2 S1 +
 //     2 xc U1 + U4, with the U sums accumulated under band-relative y
-//     weights (see sweep()); ~21 FP64 ops per grid pixel.
+//     weights (see sweep()); ~20 FP64 ops per grid pixel.
 //   * Per pair the 256 per-thread sums are reduced through shared memory in
 //     a fixed tree (the dead previous-frame buffer is the scratch), giving one
 //     partial per band; moments_finalize adds the band partials in a fixed
@@ -111,16 +111,22 @@ struct Smem {  // NB = frame-band buffers in the TMA ring (NB - 2 frames in flig
 // One thread's sweep down its column of the band for one frame pair (A, B):
 // m = {S1..S6, U1'..U4'} over the grid rows whose band-local frame row r lies
 // in [r_beg, r_end].  The y weights are relative to the band's first grid row
-// (w = r - 1, a compile-time constant per unrolled row), so row 1 needs no U
-// terms and no running coordinate is carried; the caller shifts them by the
-// absolute coordinate yc0 of that row: U1 = yc0 S2 + U1', U2 = yc0 S3 + U2',
-// U3 = yc0 S5 + U3', U4 = yc0^2 S3 + 2 yc0 U2' + U4'.
+// (w = r - 1), so no running coordinate is carried; the caller shifts them by
+// the absolute coordinate yc0 of that row: U1 = yc0 S2 + U1', U2 = yc0 S3 +
+// U2', U3 = yc0 S5 + U3', U4 = yc0^2 S3 + 2 yc0 U2' + U4'.
+// The weighted sums use running sums of the running sums instead of a
+// multiply per row: with K = BR rows, Q = sum_k S(k) (S after row k) is
+// sum_r (K - r + 1) t_r and QQ = sum_k Q(k) is sum_r (K-r+1)(K-r+2)/2 t_r, so
+//   sum_r (r-1) t_r   = K S - Q,
+//   sum_r (r-1)^2 t_r = K^2 S - (2K + 1) Q + 2 QQ      (t = ey^2 for QQ);
+// four adds per row replace one multiply and four FMAs.  Rows outside
+// [r_beg, r_end] leave S unchanged (t_r = 0) but still advance Q and QQ.
 // CHECK=false is the interior fast path (all rows, no per-row tests).
 template <typename T, int BR, bool CHECK>
 __device__ __forceinline__ void sweep(const T* __restrict__ A, const T* __restrict__ B, int col, int r_beg,
                                       int r_end, typename AccT<T>::type (&m)[10]) {
   using ACC = typename AccT<T>::type;
-  ACC s1 = 0, s2 = 0, s3 = 0, s4 = 0, s5 = 0, s6 = 0, u1 = 0, u2 = 0, u3 = 0, u4 = 0;
+  ACC s1 = 0, s2 = 0, s3 = 0, s4 = 0, s5 = 0, s6 = 0, q2 = 0, q3 = 0, q5 = 0, qq3 = 0;
   ACC hP, dP, sD;
   {
     const ACC a0 = (ACC)A[col], a1 = (ACC)A[col + 1], b0 = (ACC)B[col], b1 = (ACC)B[col + 1];
@@ -146,20 +152,28 @@ __device__ __forceinline__ void sweep(const T* __restrict__ A, const T* __restri
       s4 = fma(ex, et, s4);
       s5 = fma(ey, et, s5);
       s6 = fma(et, et, s6);
-      if (r >= 2) {
-        const ACC hh = r == 2 ? ey : ACC(r - 1) * ey;
-        u1 = fma(ex, hh, u1);
-        u2 = fma(ey, hh, u2);
-        u3 = fma(hh, et, u3);
-        u4 = fma(hh, hh, u4);
-      }
+    }
+    if (r == 1) {  // Q(1) = S(1), QQ(1) = Q(1)
+      q2 = s2;
+      q3 = s3;
+      q5 = s5;
+      qq3 = s3;
+    } else {
+      q2 += s2;
+      q3 += s3;
+      q5 += s5;
+      qq3 += q3;
     }
     hP = nhP;
     dP = ndP;
     sD = nsD;
   }
-  m[0] = s1; m[1] = s2; m[2] = s3; m[3] = s4; m[4] = s5;
-  m[5] = s6; m[6] = u1; m[7] = u2; m[8] = u3; m[9] = u4;
+  constexpr ACC K = ACC(BR);
+  m[0] = s1; m[1] = s2; m[2] = s3; m[3] = s4; m[4] = s5; m[5] = s6;
+  m[6] = fma(K, s2, -q2);
+  m[7] = fma(K, s3, -q3);
+  m[8] = fma(K, s5, -q5);
+  m[9] = fma(K * K, s3, fma(-(2 * K + 1), q3, 2 * qq3));
 }
 
 template <typename T, int BR, int NB>
