@@ -215,6 +215,10 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
+DP_PER_PX = 20 + 7 / 16
+FP64_LANE_PEAK = 32.2e12 / 2
+
+
 def time_moments_kernel(frames, steps):
     """Live CUDA-event timing of the dominant kernel launch (ct_ttc_moments on the bench input)."""
     import torch
@@ -378,8 +382,14 @@ def main():
             "traffic": traffic, "traffic_unit": "bytes/launch (dram read+write, ncu --set full, profiles/)",
             "algorithmic_bytes_per_launch": V * (NFRAMES - 1) * BYTES_PER_EST, "kernel": "ttc_moments_kernel<double> (+ finalize)", "peak_kind": peak_kind,
             "kernel_ms": t_k * 1e3, "step_ms": dt / args.steps * 1e3,
-            "fp64_pipe": {"dp_ops_per_grid_px": 20, "achieved_tflops": 2 * 20 * V * (NFRAMES - 1) * 255 * 255 / t_k / 1e12 / 2,
-                          "peak_tflops": 32.2, "peak_note": "DFMA-chain microbenchmark on the box (tools/fp_peak.cu)"}}
+            # the kernel is FP64-issue bound (profiles/r01_moments_probe.md): 20 FP64
+            # instructions per grid pixel + 7 per band-halo row (16-row bands)
+            "fp64_pipe": {"dp_instr_per_grid_px": DP_PER_PX,
+                          "achieved_lane_ops_per_s": DP_PER_PX * V * (NFRAMES - 1) * 255 * 255 / t_k,
+                          "peak_lane_ops_per_s": FP64_LANE_PEAK,
+                          "frac": DP_PER_PX * V * (NFRAMES - 1) * 255 * 255 / t_k / FP64_LANE_PEAK,
+                          "peak_note": "32.2 TFLOP/s DFMA microbenchmark on the box (tools/fp_peak.cu) = 1.61e13 lane-ops/s"},
+            "hbm_read_only_probe_gbs": 7500, "hbm_read_only_note": "TMA stream of the same boxes/ring/grid without compute (tools/tma_stream2.cu); above the copy peak"}
 
     # end to end through the public host API: pinned frames in, estimates out
     Ve = min(args.e2e_videos, V)

@@ -22,6 +22,7 @@
 //  * xcorr_generic<T>: any rank <= CT_MAXDIM and any kernel width; one thread
 //    per output, odometer over taps.  Used for ranks >= 4 and widths without
 //    a tiled instantiation.
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -598,6 +599,268 @@ int launch_tma3d(const TileArgs& a0, const T* taps_host, int ntaps, cudaStream_t
   return rc;
 }
 
+// ---------------------------------------------------------------------------
+// 3-D z-walking correlation (large 3-D kernels, BASELINE config 3).
+// Work item = one output slice of one (BY x BX) output column block.  The
+// kernel is persistent: CTA c takes items [c*per_cta, (c+1)*per_cta) of the
+// flattened (volume, tile row, tile column, z) order, i.e. one or two runs of
+// consecutive output slices, so every SM gets the same number of slices.
+// For a run [z0, z1) the CTA streams the input z-slices that feed it through
+// a TMA ring (4-D map, zero-filled halos).  Every staged slice s is used by
+// all NZ kernel planes at once: register slot j holds output z = s + pz - j,
+// so slot j accumulates plane j of the kernel from this slice; after the
+// slice, slot NZ-1 is complete (stored) and the slots shift by one.  Kernel
+// indices (j0 = slot, j2) are compile-time and j1 is a short loop, so the
+// taps come from the parameter bank with a uniform offset, and each staged
+// value feeds NZ * TY * NW FMAs.  Per output the taps are still applied in
+// row-major (j0, j1, j2) order from 0.0, so fp64 results are bit-exact.
+template <typename T, int NZ, int NH, int NW, int TY, int VX, int LW, int MAXT>
+__global__ void __launch_bounds__(MAXT, 1) xcorr_zwalk(const TileArgs a, const __grid_constant__ TapsParam<T> taps,
+                                                      const __grid_constant__ CUtensorMap tmap, int pxa,
+                                                      int64_t per_cta) {
+  extern __shared__ __align__(128) unsigned char smem_zw[];
+  constexpr int NS = 3;                             // TMA ring stages
+  constexpr int CW = VX + NW - 1;                   // window columns per row
+  constexpr int CHL = (CW + LW - 1) / LW;           // loads per window row
+  constexpr int KP = (NW * sizeof(T) + 15) / 16 * 16 / sizeof(T);  // padded taps per kernel row
+  using L = typename LoadT<T, LW>::type;
+  const int tid = threadIdx.x;
+  const int tx = tid % a.txn, ty = tid / a.txn;
+  const int BX = a.txn * VX, BY = a.tyn * TY;
+  const int tiles_x = (a.ox + BX - 1) / BX, tiles_y = (a.oy + BY - 1) / BY;
+  const int sh = pxa - a.px;
+  const size_t stage_bytes = ((size_t)a.sx * a.sy * sizeof(T) + 127) & ~size_t(127);
+  auto stage = [&](int s) { return reinterpret_cast<T*>(smem_zw + (size_t)s * stage_bytes); };
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_zw + NS * stage_bytes);
+  const uint32_t box_bytes = (uint32_t)(a.sx * a.sy * sizeof(T));
+  const bool active = ty < a.tyn;
+  const int64_t total = a.batch * tiles_y * tiles_x * (int64_t)a.oz;
+  int64_t pos = (int64_t)blockIdx.x * per_cta;
+  const int64_t end = min(total, pos + per_cta);
+  if (tid == 0) {
+    for (int i = 0; i < NS; ++i) mbar_init(&bars[i], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  int gcount = 0;  // slices consumed by this CTA: ring stage g % NS, phase (g / NS) & 1
+
+  while (pos < end) {
+    const int64_t col = pos / a.oz;
+    const int z0 = (int)(pos - col * a.oz);
+    const int64_t left = end - pos;
+    const int z1 = left < (int64_t)(a.oz - z0) ? z0 + (int)left : a.oz;
+    pos += z1 - z0;
+    const int b = (int)(col / (tiles_x * tiles_y));
+    const int tt = (int)(col - (int64_t)b * tiles_x * tiles_y);
+    const int x0 = (tt % tiles_x) * BX, y0 = (tt / tiles_x) * BY;
+    // walk slices s in [z0 - pz, z1 - 1 - pz + NZ - 1]; real ones are [g_lo, g_hi)
+    const int s_beg = z0 - a.pz, s_end = z1 - a.pz + NZ - 1;
+    const int g_lo = max(0, s_beg), g_hi = min(a.mz, s_end);
+    const int nsl = max(0, g_hi - g_lo);
+    const int g0 = gcount;
+    auto issue = [&](int k) {
+      if (tid == 0) {
+        const int st = (g0 + k) % NS;
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&bars[st], box_bytes);
+        tma_load_4d(stage(st), &tmap, &bars[st], x0 - pxa, y0 - a.py, g_lo + k, b);
+      }
+    };
+    for (int k = 0; k < NS && k < nsl; ++k) issue(k);
+
+    T acc[NZ][TY][VX];
+#pragma unroll
+    for (int j = 0; j < NZ; ++j)
+#pragma unroll
+      for (int yi = 0; yi < TY; ++yi)
+#pragma unroll
+        for (int x = 0; x < VX; ++x) acc[j][yi][x] = T(0);
+
+    T* out = reinterpret_cast<T*>(a.out) + (int64_t)b * a.oz * a.oy * a.ox;
+    const int ox = x0 + tx * VX;
+    for (int s = s_beg; s < s_end; ++s) {
+      if (s >= g_lo && s < g_hi) {
+        const int k = s - g_lo;
+        const int g = g0 + k;
+        mbar_wait(&bars[g % NS], (uint32_t)((g / NS) & 1));
+        // slot j is live for this run when its output z = s + pz - j is in [z0, z1)
+        const int jlo = max(0, s + a.pz - z1 + 1), jhi = min(NZ - 1, s + a.pz - z0);
+        const T* tile = stage(g % NS) + (ty * TY) * a.sx + sh + tx * VX;
+        if (active) {
+#pragma unroll 1
+          for (int j1 = 0; j1 < NH; ++j1) {
+            T v[TY][CHL * LW];
+#pragma unroll
+            for (int yi = 0; yi < TY; ++yi) {
+              const T* rp = tile + (yi + j1) * a.sx;
+#pragma unroll
+              for (int c = 0; c < CHL; ++c) {
+                const L q = *reinterpret_cast<const L*>(rp + c * LW);
+                const T* qp = reinterpret_cast<const T*>(&q);
+#pragma unroll
+                for (int e = 0; e < LW; ++e) v[yi][c * LW + e] = qp[e];
+              }
+            }
+            // taps padded to KP per kernel row: 16-byte groups load as one uniform vector
+            const T* kj1 = taps.v + j1 * KP;
+            auto plane = [&](int j) {
+              using V16 = typename LoadT<T, 16 / sizeof(T)>::type;
+              constexpr int G = 16 / sizeof(T);
+              T kr[KP];
+#pragma unroll
+              for (int q = 0; q < KP; q += G)
+                *reinterpret_cast<V16*>(kr + q) = *reinterpret_cast<const V16*>(kj1 + j * NH * KP + q);
+#pragma unroll
+              for (int j2 = 0; j2 < NW; ++j2) {
+                const T kv = kr[j2];
+#pragma unroll
+                for (int yi = 0; yi < TY; ++yi)
+#pragma unroll
+                  for (int x = 0; x < VX; ++x) acc[j][yi][x] = fmadd(kv, v[yi][x + j2], acc[j][yi][x]);
+              }
+            };
+            if (jlo == 0 && jhi == NZ - 1) {  // interior slice: branch-free, all slots interleavable
+#pragma unroll
+              for (int j = 0; j < NZ; ++j) plane(j);
+            } else {
+#pragma unroll
+              for (int j = 0; j < NZ; ++j)
+                if (j >= jlo && j <= jhi) plane(j);
+            }
+          }
+        }
+        __syncthreads();  // stage consumed
+        if (k + NS < nsl) issue(k + NS);
+      }
+      // slot NZ-1 now holds output z = s + pz - (NZ-1), complete
+      const int zo = s + a.pz - (NZ - 1);
+      if (zo >= z0 && zo < z1 && active) {
+#pragma unroll
+        for (int yi = 0; yi < TY; ++yi) {
+          const int y = y0 + ty * TY + yi;
+          if (y >= a.oy) break;
+          T* orow = out + ((int64_t)zo * a.oy + y) * a.ox;
+#pragma unroll
+          for (int x = 0; x < VX; ++x)
+            if (ox + x < a.ox) orow[ox + x] = acc[NZ - 1][yi][x];
+        }
+      }
+#pragma unroll
+      for (int j = NZ - 1; j > 0; --j)
+#pragma unroll
+        for (int yi = 0; yi < TY; ++yi)
+#pragma unroll
+          for (int x = 0; x < VX; ++x) acc[j][yi][x] = acc[j - 1][yi][x];
+#pragma unroll
+      for (int yi = 0; yi < TY; ++yi)
+#pragma unroll
+        for (int x = 0; x < VX; ++x) acc[0][yi][x] = T(0);
+    }
+    gcount += nsl;
+  }
+}
+
+// Output tile for the z-walking kernel: threads txn x tyn (<= 256) minimising
+// padded outputs plus staged halo over the (oy, ox) plane.
+inline void choose_zwalk_tile(int oy, int ox, int vx, int ty_rows, int nh, int nw, int* txn, int* tyn,
+                              int maxt = 256) {
+  double best = 1e300;
+  for (int tx = 16; tx <= 64; ++tx) {  // >= 16: a warp spans at most two staged rows (conflict-free LDS)
+    for (int ty = 1; tx * ty <= maxt; ++ty) {
+      if (tx * ty < maxt / 2) continue;
+      const int bx = tx * vx, by = ty * ty_rows;
+      if (bx + nw + 8 > 256 || by + nh - 1 > 256) continue;
+      const double tiles = (double)cdiv(ox, bx) * (double)cdiv(oy, by);
+      const double warps = (double)cdiv(tx * ty, 32) * 32;
+      const double cost = tiles * (warps * vx * ty_rows * (double)nh * nw + 2.0 * (bx + nw) * (by + nh));
+      if (cost < best * 0.999) {
+        best = cost;
+        *txn = tx;
+        *tyn = ty;
+      }
+    }
+  }
+}
+
+// z-chunk length for the z-walking kernels: minimise (waves of one CTA per
+// SM) x (per-CTA time ~ zc + staging/fill overhead of the NZ-1 extra slices).
+inline int zwalk_chunk(int oz, int nz, int64_t plane_ctas, int per_sm = 1) {
+  const int64_t sms = (int64_t)num_sms() * std::max(1, per_sm);
+  int best_zc = oz;
+  double best = 1e300;
+  for (int tz = 1; tz <= oz; ++tz) {
+    const int zc = (int)cdiv(oz, tz);
+    if (tz > 1 && zc == (int)cdiv(oz, tz - 1)) continue;
+    const int64_t ctas = plane_ctas * cdiv(oz, zc);
+    if (ctas > 65535 * 64) break;
+    const double waves = (double)cdiv(ctas, sms);
+    const double cost = waves * (zc + 0.15 * (zc + nz - 1) + 2.0);
+    if (cost < best * 0.999) {
+      best = cost;
+      best_zc = zc;
+    }
+  }
+  return best_zc;
+}
+
+template <typename T, int NZ, int NH, int NW, int TY, int VX, int MAXT = 256>
+int launch_zwalk(const TileArgs& a0, const T* taps_host, int ntaps, int zc_hint, cudaStream_t st) {
+  TileArgs a = a0;
+  constexpr int KP = (NW * sizeof(T) + 15) / 16 * 16 / sizeof(T);
+  static_assert(NZ * NH * KP <= MaxTaps<T>::value, "padded taps exceed the parameter block");
+  TapsParam<T> taps;
+  for (int r = 0; r < NZ * NH; ++r)
+    for (int j2 = 0; j2 < KP; ++j2) taps.v[r * KP + j2] = j2 < NW ? taps_host[r * NW + j2] : T(0);
+  (void)ntaps;
+  constexpr int VW = 16 / sizeof(T);
+  if (a.txn <= 0 || a.tyn <= 0 || a.txn * a.tyn > MAXT) choose_zwalk_tile(a.oy, a.ox, VX, TY, NH, NW, &a.txn, &a.tyn, MAXT);
+  if (getenv("CT_ZW_TXN") && getenv("CT_ZW_TYN")) {  // probing only
+    a.txn = atoi(getenv("CT_ZW_TXN"));
+    a.tyn = atoi(getenv("CT_ZW_TYN"));
+  }
+  const int pxa = (a.px + VW - 1) / VW * VW;
+  const int sh = pxa - a.px;
+  const int BX = a.txn * VX, BY = a.tyn * TY;
+  a.sx = (sh + BX + NW - 1 + VW - 1) / VW * VW;
+  a.sy = BY + NH - 1;
+  const size_t stage_bytes = ((size_t)a.sx * a.sy * sizeof(T) + 127) & ~size_t(127);
+  const size_t smem = 3 * stage_bytes + 64;
+  CT_REQUIRE(smem <= 227 * 1024, "zwalk tile too large");
+  const int nthr = (int)cdiv(a.txn * a.tyn, 32) * 32;
+  void (*kern)(const TileArgs, const TapsParam<T>, const CUtensorMap, int, int64_t);
+  if (VW == 4 && sh % 4 == 0 && VX % 4 == 0)
+    kern = xcorr_zwalk<T, NZ, NH, NW, TY, VX, (VW == 4 ? 4 : 2), MAXT>;
+  else if (sh % 2 == 0)
+    kern = xcorr_zwalk<T, NZ, NH, NW, TY, VX, 2, MAXT>;
+  else
+    kern = xcorr_zwalk<T, NZ, NH, NW, TY, VX, 1, MAXT>;
+  CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 1;
+  CT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nthr, smem));
+  // persistent: the flattened (volume, tile, z) output slices split evenly
+  // over every resident CTA slot (runs shorter than 2 NZ slices waste staging)
+  const int64_t total = cdiv(a.ox, BX) * cdiv(a.oy, BY) * a.batch * a.oz;
+  const int64_t slots = (int64_t)num_sms() * std::max(1, per_sm);
+  int64_t per_cta = std::max<int64_t>(cdiv(total, slots), 2 * NZ);
+  if (zc_hint > 0) per_cta = zc_hint;
+  if (const char* e = getenv("CT_ZW_ZC")) per_cta = std::max(1, atoi(e));  // probing only
+  const int64_t nctas = cdiv(total, per_cta);
+  CT_REQUIRE(nctas < (1ll << 31), "too many z-walk CTAs");
+  CUtensorMap tmap;
+  memset(&tmap, 0, sizeof(tmap));
+  if (a.sx > 256 || a.sy > 256 ||
+      !encode_tmap_4d(&tmap, a.s, sizeof(T), (uint64_t)a.mx, (uint64_t)a.my, (uint64_t)a.mz, (uint64_t)a.batch, a.sx,
+                      a.sy)) {
+    set_error("tensor map encode failed");
+    return CT_EUNSUPPORTED;
+  }
+  if (getenv("CT_DEBUG"))
+    fprintf(stderr, "xcorr_zwalk TY %d MAXT %d: tile %dx%d (%d thr) per_cta %lld per_sm %d ctas %lld smem %zu\n", TY,
+            MAXT, BX, BY, nthr, (long long)per_cta, per_sm, (long long)nctas, smem);
+  kern<<<(unsigned)nctas, nthr, smem, st>>>(a, taps, tmap, pxa, per_cta);
+  return check_launch("xcorr_zwalk");
+}
+
 template <typename T, int NW, int VX, int TY, int TZ>
 int launch_tiled(const TileArgs& a0, const T* k_host_order_taps, int ntaps, cudaStream_t st) {
   TileArgs a = a0;
@@ -634,7 +897,7 @@ struct TapsPairParam {
 
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
   unsigned long long r;
-  asm volatile("fma.rn.f32x2 %0, %1, %2, %3;"
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
       : "=l"(r)
       : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
         "l"(*reinterpret_cast<unsigned long long*>(&c)));
@@ -786,6 +1049,190 @@ int launch_pair_f32(const TileArgs& a0, const float* taps_host, int ntaps, cudaS
   return check_launch("xcorr_pair_f32");
 }
 
+// fp32 z-walking kernel with packed FFMA2: the accumulators are (x, x+1)
+// float2 pairs and the taps (k, k) pairs in the parameter bank, so one
+// FFMA2 does two output FMAs.  A row's window pairs (v[j2+x], v[j2+x+1]) are
+// 8-byte aligned in the staged slice for one parity of j2 and in a copy of
+// the slice shifted by one element for the other (built in shared memory
+// after each TMA lands), so every operand is a single 64-bit load.
+template <int NZ, int NH, int NW, int TY, int ODD, int MAXT>
+__global__ void __launch_bounds__(MAXT, 1) xcorr_zwalk_x2(const TileArgs a, const __grid_constant__ TapsPairParam taps,
+                                                         const __grid_constant__ CUtensorMap tmap, int pxa, int zc) {
+  extern __shared__ __align__(128) unsigned char smem_zw2[];
+  constexpr int NS = 3;
+  constexpr int VX = 4;
+  constexpr int NPE = (VX + NW - 1 + 1) / 2;  // aligned pairs per window row
+  constexpr int NPO = (VX + NW - 2) / 2;      // shifted pairs per window row
+  const int tid = threadIdx.x;
+  const int nthr = blockDim.x;
+  const int tx = tid % a.txn, ty = tid / a.txn;
+  const int BX = a.txn * VX, BY = a.tyn * TY;
+  const int x0 = blockIdx.x * BX, y0 = blockIdx.y * BY;
+  const int sh = pxa - a.px;
+  const int plane = a.sx * a.sy;
+  const size_t stage_bytes = ((size_t)plane * sizeof(float) + 127) & ~size_t(127);
+  auto stage = [&](int s) { return reinterpret_cast<float*>(smem_zw2 + (size_t)s * stage_bytes); };
+  float* shifted = reinterpret_cast<float*>(smem_zw2 + NS * stage_bytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_zw2 + (NS + 1) * stage_bytes);
+  const uint32_t box_bytes = (uint32_t)(plane * sizeof(float));
+  const bool active = ty < a.tyn;
+  const int b = (int)(blockIdx.z / a.tiles_z);
+  const int z0 = (int)(blockIdx.z % a.tiles_z) * zc;
+  const int z1 = min(z0 + zc, a.oz);
+  const int s_beg = z0 - a.pz, s_end = z1 - a.pz + NZ - 1;
+  const int g_lo = max(0, s_beg), g_hi = min(a.mz, s_end);
+  const int nsl = max(0, g_hi - g_lo);
+  if (tid == 0) {
+    for (int i = 0; i < NS; ++i) mbar_init(&bars[i], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  auto issue = [&](int k) {
+    if (tid == 0) {
+      fence_proxy_async_smem();
+      mbar_arrive_expect_tx(&bars[k % NS], box_bytes);
+      tma_load_4d(stage(k % NS), &tmap, &bars[k % NS], x0 - pxa, y0 - a.py, g_lo + k, b);
+    }
+  };
+  for (int k = 0; k < NS && k < nsl; ++k) issue(k);
+
+  float2 acc[NZ][TY][VX / 2];
+#pragma unroll
+  for (int j = 0; j < NZ; ++j)
+#pragma unroll
+    for (int yi = 0; yi < TY; ++yi)
+#pragma unroll
+      for (int x = 0; x < VX / 2; ++x) acc[j][yi][x] = make_float2(0.f, 0.f);
+
+  float* out = reinterpret_cast<float*>(a.out) + (int64_t)b * a.oz * a.oy * a.ox;
+  const int ox = x0 + tx * VX;
+  // window base element of this thread; ODD = base parity (sh parity)
+  const int wb = (ty * TY) * a.sx + sh + tx * VX;
+  for (int s = s_beg; s < s_end; ++s) {
+    if (s >= g_lo && s < g_hi) {
+      const int k = s - g_lo;
+      mbar_wait(&bars[k % NS], (uint32_t)((k / NS) & 1));
+      const float* tile = stage(k % NS);
+      for (int i = tid; i < plane - 1; i += nthr) shifted[i] = tile[i + 1];
+      __syncthreads();
+      const int jlo = max(0, s + a.pz - z1 + 1), jhi = min(NZ - 1, s + a.pz - z0);
+      if (active) {
+        // pairs starting at window offset 2m (E) and 2m+1 (O)
+        const float* srcE = ODD ? shifted + wb - 1 : tile + wb;
+        const float* srcO = ODD ? tile + wb + 1 : shifted + wb;
+#pragma unroll 1
+        for (int j1 = 0; j1 < NH; ++j1) {
+          float2 pe[TY][NPE], po[TY][NPO > 0 ? NPO : 1];
+#pragma unroll
+          for (int yi = 0; yi < TY; ++yi) {
+            const int ro = (yi + j1) * a.sx;
+#pragma unroll
+            for (int m = 0; m < NPE; ++m) pe[yi][m] = *reinterpret_cast<const float2*>(srcE + ro + 2 * m);
+#pragma unroll
+            for (int m = 0; m < NPO; ++m) po[yi][m] = *reinterpret_cast<const float2*>(srcO + ro + 2 * m);
+          }
+          const float2* kj1 = taps.v + j1 * NW;
+          auto plane = [&](int j) {
+            const float2* kr = kj1 + j * NH * NW;
+#pragma unroll
+            for (int j2 = 0; j2 < NW; ++j2) {
+              const float2 kk = kr[j2];
+#pragma unroll
+              for (int yi = 0; yi < TY; ++yi)
+#pragma unroll
+                for (int xp = 0; xp < VX / 2; ++xp) {
+                  const int e = 2 * xp + j2;  // window offset of the pair
+                  const float2 w = (e & 1) ? po[yi][e >> 1] : pe[yi][e >> 1];
+                  acc[j][yi][xp] = ffma2(kk, w, acc[j][yi][xp]);
+                }
+            }
+          };
+          if (jlo == 0 && jhi == NZ - 1) {  // interior slice: branch-free, all slots interleavable
+#pragma unroll
+            for (int j = 0; j < NZ; ++j) plane(j);
+          } else {
+#pragma unroll
+            for (int j = 0; j < NZ; ++j)
+              if (j >= jlo && j <= jhi) plane(j);
+          }
+        }
+      }
+      __syncthreads();  // stage and shifted copy consumed
+      if (k + NS < nsl) issue(k + NS);
+    }
+    const int zo = s + a.pz - (NZ - 1);
+    if (zo >= z0 && zo < z1 && active) {
+#pragma unroll
+      for (int yi = 0; yi < TY; ++yi) {
+        const int y = y0 + ty * TY + yi;
+        if (y >= a.oy) break;
+        float* orow = out + ((int64_t)zo * a.oy + y) * a.ox;
+#pragma unroll
+        for (int xp = 0; xp < VX / 2; ++xp) {
+          if (ox + 2 * xp < a.ox) orow[ox + 2 * xp] = acc[NZ - 1][yi][xp].x;
+          if (ox + 2 * xp + 1 < a.ox) orow[ox + 2 * xp + 1] = acc[NZ - 1][yi][xp].y;
+        }
+      }
+    }
+#pragma unroll
+    for (int j = NZ - 1; j > 0; --j)
+#pragma unroll
+      for (int yi = 0; yi < TY; ++yi)
+#pragma unroll
+        for (int x = 0; x < VX / 2; ++x) acc[j][yi][x] = acc[j - 1][yi][x];
+#pragma unroll
+    for (int yi = 0; yi < TY; ++yi)
+#pragma unroll
+      for (int x = 0; x < VX / 2; ++x) acc[0][yi][x] = make_float2(0.f, 0.f);
+  }
+}
+
+template <int NZ, int NH, int NW, int TY, int MAXT = 256>
+int launch_zwalk_x2(const TileArgs& a0, const float* taps_host, int ntaps, cudaStream_t st) {
+  TileArgs a = a0;
+  TapsPairParam taps;
+  for (int i = 0; i < ntaps; ++i) taps.v[i] = make_float2(taps_host[i], taps_host[i]);
+  constexpr int VX = 4;
+  if (a.txn <= 0 || a.tyn <= 0 || a.txn * a.tyn > MAXT) choose_zwalk_tile(a.oy, a.ox, VX, TY, NH, NW, &a.txn, &a.tyn, MAXT);
+  if (getenv("CT_ZW_TXN") && getenv("CT_ZW_TYN")) {  // probing only
+    a.txn = atoi(getenv("CT_ZW_TXN"));
+    a.tyn = atoi(getenv("CT_ZW_TYN"));
+  }
+  const int pxa = (a.px + 3) / 4 * 4;
+  const int sh = pxa - a.px;
+  const int BX = a.txn * VX, BY = a.tyn * TY;
+  a.sx = (sh + BX + NW - 1 + 1 + 3) / 4 * 4;  // +1: the shifted copy's last pair
+  a.sy = BY + NH - 1;
+  const size_t stage_bytes = ((size_t)a.sx * a.sy * sizeof(float) + 127) & ~size_t(127);
+  const size_t smem = 4 * stage_bytes + 64;
+  CT_REQUIRE(smem <= 227 * 1024, "zwalk tile too large");
+  const int nthr = (int)cdiv(a.txn * a.tyn, 32) * 32;
+  void (*kern)(const TileArgs, const TapsPairParam, const CUtensorMap, int, int);
+  if (sh & 1)
+    kern = xcorr_zwalk_x2<NZ, NH, NW, TY, 1, MAXT>;
+  else
+    kern = xcorr_zwalk_x2<NZ, NH, NW, TY, 0, MAXT>;
+  CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 1;
+  CT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nthr, smem));
+  const int64_t plane_ctas = cdiv(a.ox, BX) * cdiv(a.oy, BY) * a.batch;
+  int zc = zwalk_chunk(a.oz, NZ, plane_ctas, per_sm);
+  if (const char* e = getenv("CT_ZW_ZC")) zc = std::max(1, atoi(e));  // probing only
+  a.tiles_z = (int)cdiv(a.oz, zc);
+  CT_REQUIRE(a.batch * a.tiles_z <= 65535, "too many z chunks");
+  CUtensorMap tmap;
+  memset(&tmap, 0, sizeof(tmap));
+  if (a.sx > 256 || a.sy > 256 ||
+      !encode_tmap_4d(&tmap, a.s, sizeof(float), (uint64_t)a.mx, (uint64_t)a.my, (uint64_t)a.mz, (uint64_t)a.batch,
+                      a.sx, a.sy)) {
+    set_error("tensor map encode failed");
+    return CT_EUNSUPPORTED;
+  }
+  dim3 grid((unsigned)cdiv(a.ox, BX), (unsigned)cdiv(a.oy, BY), (unsigned)(a.batch * a.tiles_z));
+  kern<<<grid, nthr, smem, st>>>(a, taps, tmap, pxa, zc);
+  return check_launch("xcorr_zwalk_x2");
+}
+
 // Tile shape (threads along x, thread rows) minimising padded FMAs plus
 // staging over the whole output, for vx outputs per thread along x and
 // rows_per_thread output rows per thread.
@@ -873,6 +1320,41 @@ int launch_variant(TileArgs a, int kind, int nw, bool is3d, int txn, int tyn, co
     set_error("unsupported kernel width %d", nw);
     return CT_EUNSUPPORTED;
   }
+  if constexpr (sizeof(T) == 4) {
+    if (kind == 5) {  // z-walking 3-D kernel with packed FFMA2 (fp32)
+      const int n = a.nz;
+      const float* tf = reinterpret_cast<const float*>(taps);
+      const int cfg = getenv("CT_ZW_CFG") ? atoi(getenv("CT_ZW_CFG")) : 2;
+      if (n == a.ny && n == nw) {
+#define CT_ZWN(N)                                                                      \
+  if (n == N) {                                                                        \
+    if (cfg == 0) return launch_zwalk_x2<N, N, N, 4, 256>(a, tf, ntaps, st);           \
+    return launch_zwalk_x2<N, N, N, 2, 512>(a, tf, ntaps, st);                         \
+  }
+        CT_ZWN(3) CT_ZWN(5) CT_ZWN(7)
+#undef CT_ZWN
+      }
+      set_error("z-walk kernel needs a 3x3x3, 5x5x5 or 7x7x7 kernel");
+      return CT_EUNSUPPORTED;
+    }
+  }
+  if (kind == 4) {  // z-walking 3-D kernel (zero boundary, aligned rows, cubic 3/5/7 kernels; see zwalk_ok)
+    constexpr int ZVX = sizeof(T) == 4 ? 4 : 2;
+    const int n = a.nz;
+    const int cfg = getenv("CT_ZW_CFG") ? atoi(getenv("CT_ZW_CFG")) : 2;
+    if (n == a.ny && n == nw) {
+#define CT_ZWN(N)                                                                          \
+  if (n == N) {                                                                            \
+    if (cfg == 1) return launch_zwalk<T, N, N, N, 3, ZVX, 384>(a, taps, ntaps, 0, st);    \
+    if (cfg == 2) return launch_zwalk<T, N, N, N, 2, ZVX, 512>(a, taps, ntaps, 0, st);    \
+    return launch_zwalk<T, N, N, N, 4, ZVX, 256>(a, taps, ntaps, 0, st);                   \
+  }
+      CT_ZWN(3) CT_ZWN(5) CT_ZWN(7)
+#undef CT_ZWN
+    }
+    set_error("z-walk kernel needs a 3x3x3, 5x5x5 or 7x7x7 kernel");
+    return CT_EUNSUPPORTED;
+  }
   if (kind == 3) {  // TMA-staged 3-D kernel (zero boundary, aligned rows; see tma3_ok)
     switch (nw) {
 #define CT_CASE(W) case W: return launch_tma3d<T, W, VX, 4, 2>(a, taps, ntaps, st);
@@ -948,6 +1430,14 @@ int run_tiled_autotuned(TileArgs a, int nw, bool is3d, const T* taps, int ntaps,
       const int sx = (vw + v.txn * VX + nw - 1 + vw - 1) / vw * vw, sy = v.tyn * 4 + a.ny - 1;
       if (sx <= 256 && sy <= 256 && 2 * (size_t)sx * sy * sizeof(T) + 512 <= 227 * 1024) cands.push_back(v);
     }
+  }
+  // z-walking 3-D kernel: same TMA conditions, cubic 3/5/7 kernels
+  const bool zwalk_ok = tma3_ok && a.nz == a.ny && a.ny == nw && (nw == 3 || nw == 5 || nw == 7);
+  if (zwalk_ok) {
+    int zx = 0, zy = 0;
+    choose_zwalk_tile(a.oy, a.ox, sizeof(T) == 4 ? 4 : 2, 4, a.ny, nw, &zx, &zy);
+    cands.insert(cands.begin(), Variant{4, zx, zy});
+    if (sizeof(T) == 4) cands.insert(cands.begin(), Variant{5, zx, zy});
   }
   const double work = (double)a.batch * a.oz * a.oy * a.ox * (double)a.nz * a.ny * nw;
   static const bool tune = !(getenv("CT_CONV_AUTOTUNE") && atoi(getenv("CT_CONV_AUTOTUNE")) == 0);

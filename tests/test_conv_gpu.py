@@ -226,7 +226,7 @@ def test_each_kernel_variant_matches_oracle(kind, monkeypatch):
             assert rel_inf(g32[i], ref) <= 1e-5, (kind, ms, ns)
 
 
-@pytest.mark.parametrize("kind", ["0", "1", "3"])
+@pytest.mark.parametrize("kind", ["0", "1", "3", "4", "5"])
 def test_each_3d_kernel_variant_matches_oracle(kind, monkeypatch):
     """3-D shapes with each tiled variant pinned (3 = TMA-staged z-slices, used for
     zero extension with 16-byte rows; odd rows fall back): fp64 bit-exact, fp32 1e-5."""
@@ -234,7 +234,8 @@ def test_each_3d_kernel_variant_matches_oracle(kind, monkeypatch):
     rng = np.random.default_rng(int(kind) + 70)
     for ms, ns, shape in [((20, 33, 64), (5, 5, 5), F), ((17, 40, 36), (3, 3, 3), S),
                           ((9, 24, 32), (3, 5, 7), V), ((12, 30, 41), (3, 3, 5), F),
-                          ((6, 70, 300), (2, 4, 9), S)]:
+                          ((6, 70, 300), (2, 4, 9), S), ((30, 20, 28), (7, 7, 7), F),
+                          ((40, 12, 20), (7, 7, 7), V), ((3, 90, 76), (5, 5, 5), S)]:
         s64 = rng.random((2,) + ms)
         k64 = rng.standard_normal(ns)
         got = ct.direct_batch(torch.from_numpy(s64).cuda(), k64, shape, flip=False).cpu().numpy()
