@@ -75,13 +75,15 @@ struct MomentArgs {
 template <typename T, int BR, int NT>
 __device__ __forceinline__ void write_dec(const MomentArgs& a, const T* buf, int64_t v, int f, int gy0, int cx0,
                                           int tid) {
+  static_assert(NT % 128 == 0, "write_dec maps 128 dec columns per thread row");
   const int dy0 = gy0 >> 1, dx0 = cx0 >> 1;
   const int ndy = min(BR / 2, a.dh - dy0);
   const int ndx = min((a.tile_cols + 1) >> 1, a.dw - dx0);
-  if (ndy <= 0 || ndx <= 0) return;
-  T* dst = reinterpret_cast<T*>(a.dec) + ((v * a.n_frames + f) * (int64_t)a.dh + dy0) * a.dw + dx0;
-  for (int e = tid; e < ndy * ndx; e += NT) {
-    const int yy = e / ndx, xx = e - yy * ndx;
+  const int xx = tid & 127;  // dec column of this thread (a tile has <= 128 of them)
+  if (ndy <= 0 || xx >= ndx) return;
+  T* dst = reinterpret_cast<T*>(a.dec) + ((v * a.n_frames + f) * (int64_t)a.dh + dy0) * a.dw + dx0 + xx;
+#pragma unroll 4
+  for (int yy = tid >> 7; yy < ndy; yy += NT / 128) {
     const T* p0 = buf + (2 * yy) * kBoxCols + 2 * xx;
     const T* p1 = p0 + kBoxCols;
     T d;
@@ -90,7 +92,7 @@ __device__ __forceinline__ void write_dec(const MomentArgs& a, const T* buf, int
     } else {
       d = __fmul_rn(0.25f, __fadd_rn(__fadd_rn(__fadd_rn(p0[0], p0[1]), p1[0]), p1[1]));
     }
-    dst[(int64_t)yy * a.dw + xx] = d;
+    dst[(int64_t)yy * a.dw] = d;
   }
 }
 

@@ -26,6 +26,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "common.cuh"
 #include "moments.cuh"
@@ -370,12 +371,130 @@ int launch_pyramid(const T* in, int64_t n_images, int h, int w, T* out, cudaStre
   return check_launch("pyramid_down");
 }
 
+// Blur-only pyramid stage, register sliding window: a warp owns 32 x VX
+// consecutive columns (one 16-byte vector per lane) of a strip of rows of one
+// decimated image and walks down it; per input row the lane's horizontal
+// 5-tap sums come from its vector plus two neighbours on each side (warp
+// shuffles, direct clamped loads at the warp and image edges), the last five
+// horizontal rows stay in registers and each output row is their vertical
+// 5-tap sum.  Same tap order and FMA chains as the shared-memory version
+// (horizontal j1 = 0..4 then vertical j0 = 0..4), so results are identical.
+
+template <typename T>
+__global__ void __launch_bounds__(256) blur5_rows_kernel(const T* __restrict__ in, int64_t n_images, int dh, int dw,
+                                                         int strip, T* __restrict__ out) {
+  constexpr int VX = 16 / sizeof(T);
+  using V = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+  const T b5[5] = {T(1.0 / 16.0), T(4.0 / 16.0), T(6.0 / 16.0), T(4.0 / 16.0), T(1.0 / 16.0)};
+  const int lane = threadIdx.x & 31;
+  const int warps_x = (dw + 32 * VX - 1) / (32 * VX);
+  const int n_strips = (dh + strip - 1) / strip;
+  const int64_t total = n_images * n_strips * warps_x;
+  const int64_t wstride = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t item = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); item < total; item += wstride) {
+    const int wx = (int)(item % warps_x);
+    const int64_t t = item / warps_x;
+    const int si = (int)(t % n_strips);
+    const int64_t img = t / n_strips;
+    const int x = (wx * 32 + lane) * VX;
+    const bool valid = x < dw;
+    const int y0 = si * strip, y1 = min(dh, y0 + strip);
+    const T* src = in + img * (int64_t)dh * dw;
+    T* dst = out + img * (int64_t)dh * dw;
+    T h[5][VX];
+    // row fetch (vector + the direct edge loads of lanes 0 / 31), software
+    // pipelined one row ahead so the load latency overlaps the previous row
+    // (measured: three rows ahead is slower)
+    struct Row {
+      V q;
+      T e0, e1, e2, e3;
+    };
+    auto fetch = [&](int yy) {
+      Row r;
+      const T* srow = src + (int64_t)min(max(yy, 0), dh - 1) * dw;
+      r.q = valid ? *reinterpret_cast<const V*>(srow + x) : V{};
+      r.e0 = r.e1 = r.e2 = r.e3 = T(0);
+      if (valid && lane == 0 && x > 0) {
+        r.e0 = srow[x - 2];
+        r.e1 = srow[x - 1];
+      }
+      if (valid && lane == 31 && x + VX < dw) {
+        r.e2 = srow[x + VX];
+        r.e3 = srow[min(x + VX + 1, dw - 1)];
+      }
+      return r;
+    };
+    Row nxt = fetch(y0 - 2);
+    for (int yy = y0 - 2; yy < y1 + 2; ++yy) {
+      const Row cur = nxt;
+      if (yy + 1 < y1 + 2) nxt = fetch(yy + 1);
+      T m[VX + 4];  // columns x-2 .. x+VX+1
+      const T* qv = reinterpret_cast<const T*>(&cur.q);
+#pragma unroll
+      for (int c = 0; c < VX; ++c) m[c + 2] = qv[c];
+      m[0] = __shfl_up_sync(0xffffffffu, qv[VX - 2], 1);
+      m[1] = __shfl_up_sync(0xffffffffu, qv[VX - 1], 1);
+      m[VX + 2] = __shfl_down_sync(0xffffffffu, qv[0], 1);
+      m[VX + 3] = __shfl_down_sync(0xffffffffu, qv[1], 1);
+      if (valid) {
+        if (x == 0) {
+          m[0] = m[1] = qv[0];
+        } else if (lane == 0) {
+          m[0] = cur.e0;
+          m[1] = cur.e1;
+        }
+        if (x + VX >= dw) {
+          m[VX + 2] = m[VX + 3] = qv[VX - 1];
+        } else if (lane == 31) {
+          m[VX + 2] = cur.e2;
+          m[VX + 3] = cur.e3;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int c = 0; c < VX; ++c) h[k][c] = h[k + 1][c];
+#pragma unroll
+      for (int c = 0; c < VX; ++c) {
+        T acc = T(0);
+#pragma unroll
+        for (int j1 = 0; j1 < 5; ++j1) acc = fmx(b5[j1], m[c + j1], acc);
+        h[4][c] = acc;
+      }
+      if (yy >= y0 + 2 && valid) {
+        V o;
+        T* ov = reinterpret_cast<T*>(&o);
+#pragma unroll
+        for (int c = 0; c < VX; ++c) {
+          T acc = T(0);
+#pragma unroll
+          for (int j0 = 0; j0 < 5; ++j0) acc = fmx(b5[j0], h[j0][c], acc);
+          ov[c] = acc;
+        }
+        *reinterpret_cast<V*>(dst + (int64_t)(yy - 2) * dw + x) = o;
+      }
+    }
+  }
+}
+
 // Second half of downsample: 5x5 binomial SAME/REPLICATE over already
 // decimated images (dh x dw each, from the fused moments kernel).
 template <typename T>
 int launch_blur_dec(const T* dec, int64_t n_images, int h, int w, T* out, cudaStream_t st) {
   const int dh = h / 2, dw = w / 2;
   if (n_images == 0 || dh == 0 || dw == 0) return CT_OK;
+  constexpr int VX = 16 / sizeof(T);
+  if (dw % VX == 0 && reinterpret_cast<uintptr_t>(dec) % 16 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0 &&
+      !getenv("CT_BLUR_SMEM")) {
+    // row strips per warp: as long as possible (the 4 halo rows are re-read)
+    // while keeping >= 16 warps per SM busy
+    int strip = 64;
+    while (strip > 8 && n_images * cdiv(dh, strip) * cdiv(dw, 32 * VX) < (int64_t)num_sms() * 16) strip /= 2;
+    const int64_t items = n_images * cdiv(dh, strip) * cdiv(dw, 32 * VX);
+    const int64_t blocks = std::min<int64_t>(cdiv(items, 8), (int64_t)num_sms() * 8 * 4);
+    blur5_rows_kernel<T><<<(unsigned)blocks, 256, 0, st>>>(dec, n_images, dh, dw, strip, out);
+    return check_launch("pyramid_blur_rows");
+  }
   const int tiles = ((dh + kPyTileY - 1) / kPyTileY) * ((dw + kPyTileX - 1) / kPyTileX);
   dim3 grid((unsigned)tiles, (unsigned)std::min<int64_t>(n_images, 65535));
   pyramid_down_kernel<T, false, false><<<grid, 256, 0, st>>>(dec, n_images, h, w, out);

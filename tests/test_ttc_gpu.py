@@ -248,3 +248,16 @@ def test_batched_textures_match_single():
         assert torch.equal(batch[j], ct.make_texture(64, 48, s))
     ref = O.make_texture(64, 48, 5)
     assert np.array_equal(batch[1].cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("hw", [(270, 480), (135, 244), (66, 130), (101, 77)])
+def test_blur_register_window_matches_smem_stage(monkeypatch, dtype, hw):
+    """The register sliding-window blur (blur5_rows_kernel) and the shared-memory
+    stage it replaces use the same FMA chains: multiscale estimates must be
+    bit-identical (odd widths take the shared-memory stage either way)."""
+    f = torch.from_numpy(O.generate(hw[1], hw[0], 5, 80.0, (0.4, 0.55), 3, 0.0)).to(dtype).cuda()
+    a = ct.run_sequence_batch(f[None], max_level=3).cpu().numpy()
+    monkeypatch.setenv("CT_BLUR_SMEM", "1")
+    b = ct.run_sequence_batch(f[None], max_level=3).cpu().numpy()
+    assert np.array_equal(np.nan_to_num(a, nan=7.0), np.nan_to_num(b, nan=7.0))
