@@ -47,6 +47,10 @@ constexpr int kTileGridCols = 255;   // grid columns when the frame fits one til
 constexpr int kTileStrideMulti = 252;
 constexpr int kThreads = 256;        // one grid column per thread
 constexpr int kRedSeg = 16;          // reduction tree: 16 segments of 16 threads
+#ifndef CT_MOM_PACKED_F32
+#define CT_MOM_PACKED_F32 1
+#endif
+constexpr bool kPackedF32 = CT_MOM_PACKED_F32;  // fp32 interior bands use sweep_x2
 
 template <typename T>
 struct AccT {
@@ -178,6 +182,91 @@ __device__ __forceinline__ void sweep(const T* __restrict__ A, const T* __restri
   m[9] = fma(K * K, s3, fma(-(2 * K + 1), q3, 2 * qq3));
 }
 
+// fp32 interior sweep with packed f32x2 arithmetic: lane .x of every pair
+// register walks band rows 1..BR/2 and lane .y rows BR/2+1..BR of the same
+// column, so each FADD2/FFMA2 does the work of two scalar instructions (the
+// per-lane operation order is the scalar sweep's).  The two half-band sums
+// are combined with the y-weight shift of the second half: with H = BR/2,
+// U1 += H S2, U2 += H S3, U3 += H S5, U4 += H^2 S3 + 2 H U2 (second half).
+__device__ __forceinline__ float2 f2add(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(*reinterpret_cast<unsigned long long*>(&a)),
+      "l"(*reinterpret_cast<unsigned long long*>(&b)));
+  return *reinterpret_cast<float2*>(&r);
+}
+__device__ __forceinline__ float2 f2sub(float2 a, float2 b) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(*reinterpret_cast<unsigned long long*>(&a)),
+      "l"(*reinterpret_cast<unsigned long long*>(&b)));
+  return *reinterpret_cast<float2*>(&r);
+}
+__device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(*reinterpret_cast<unsigned long long*>(&a)),
+      "l"(*reinterpret_cast<unsigned long long*>(&b)), "l"(*reinterpret_cast<unsigned long long*>(&c)));
+  return *reinterpret_cast<float2*>(&r);
+}
+
+template <int BR>
+__device__ __forceinline__ void sweep_x2(const float* __restrict__ A, const float* __restrict__ B, int col,
+                                         float (&m)[10]) {
+  constexpr int H = BR / 2;
+  auto ld = [&](const float* F, int r, int c) { return make_float2(F[r * kBoxCols + c], F[(r + H) * kBoxCols + c]); };
+  float2 s1 = {0, 0}, s2 = {0, 0}, s3 = {0, 0}, s4 = {0, 0}, s5 = {0, 0}, s6 = {0, 0};
+  float2 q2, q3, q5, qq3, hP, dP, sD;
+  {
+    const float2 a0 = ld(A, 0, col), a1 = ld(A, 0, col + 1), b0 = ld(B, 0, col), b1 = ld(B, 0, col + 1);
+    const float2 P0 = f2add(a0, b0), P1 = f2add(a1, b1), D0 = f2sub(b0, a0), D1 = f2sub(b1, a1);
+    hP = f2add(P0, P1);
+    dP = f2sub(P1, P0);
+    sD = f2add(D0, D1);
+  }
+#pragma unroll
+  for (int r = 1; r <= H; ++r) {
+    const float2 a0 = ld(A, r, col), a1 = ld(A, r, col + 1), b0 = ld(B, r, col), b1 = ld(B, r, col + 1);
+    const float2 P0 = f2add(a0, b0), P1 = f2add(a1, b1), D0 = f2sub(b0, a0), D1 = f2sub(b1, a1);
+    const float2 nhP = f2add(P0, P1), ndP = f2sub(P1, P0), nsD = f2add(D0, D1);
+    const float2 ex = f2add(dP, ndP), ey = f2sub(nhP, hP), et = f2add(sD, nsD);
+    s1 = f2fma(ex, ex, s1);
+    s2 = f2fma(ex, ey, s2);
+    s3 = f2fma(ey, ey, s3);
+    s4 = f2fma(ex, et, s4);
+    s5 = f2fma(ey, et, s5);
+    s6 = f2fma(et, et, s6);
+    if (r == 1) {
+      q2 = s2;
+      q3 = s3;
+      q5 = s5;
+      qq3 = s3;
+    } else {
+      q2 = f2add(q2, s2);
+      q3 = f2add(q3, s3);
+      q5 = f2add(q5, s5);
+      qq3 = f2add(qq3, q3);
+    }
+    hP = nhP;
+    dP = ndP;
+    sD = nsD;
+  }
+  constexpr float K = float(H);
+  // per half: U1' = K S2 - Q2, U2' = K S3 - Q3, U3' = K S5 - Q5, U4' = K^2 S3 - (2K+1) Q3 + 2 QQ3
+  const float u1x = fmaf(K, s2.x, -q2.x), u1y = fmaf(K, s2.y, -q2.y);
+  const float u2x = fmaf(K, s3.x, -q3.x), u2y = fmaf(K, s3.y, -q3.y);
+  const float u3x = fmaf(K, s5.x, -q5.x), u3y = fmaf(K, s5.y, -q5.y);
+  const float u4x = fmaf(K * K, s3.x, fmaf(-(2 * K + 1), q3.x, 2 * qq3.x));
+  const float u4y = fmaf(K * K, s3.y, fmaf(-(2 * K + 1), q3.y, 2 * qq3.y));
+  m[0] = s1.x + s1.y;
+  m[1] = s2.x + s2.y;
+  m[2] = s3.x + s3.y;
+  m[3] = s4.x + s4.y;
+  m[4] = s5.x + s5.y;
+  m[5] = s6.x + s6.y;
+  m[6] = u1x + fmaf(K, s2.y, u1y);
+  m[7] = u2x + fmaf(K, s3.y, u2y);
+  m[8] = u3x + fmaf(K, s5.y, u3y);
+  m[9] = u4x + fmaf(K * K, s3.y, fmaf(2 * K, u2y, u4y));
+}
+
 template <typename T, int BR, int NB>
 __global__ void __launch_bounds__(kThreads, 2) ttc_moments_kernel(const MomentArgs a,
                                                                   const __grid_constant__ CUtensorMap tmap) {
@@ -258,10 +347,14 @@ __global__ void __launch_bounds__(kThreads, 2) ttc_moments_kernel(const MomentAr
       if (p1 == n_pairs && i == p1 - p0 - 1) write_dec<T, BR, kThreads>(a, B, v, p1, gy0, cx0, tid);
     }
     ACC m[10];
-    if (r_beg <= 1 && r_end >= BR)
-      sweep<T, BR, false>(A, B, tid, 1, BR, m);
-    else
+    if (r_beg <= 1 && r_end >= BR) {
+      if constexpr (sizeof(T) == 4 && kPackedF32)
+        sweep_x2<BR>(A, B, tid, m);
+      else
+        sweep<T, BR, false>(A, B, tid, 1, BR, m);
+    } else {
       sweep<T, BR, true>(A, B, tid, r_beg, r_end, m);
+    }
 
     // this thread's ten sums, order m00 m01 m02 m11 m12 m22 r0 r1 r2 et2 (rhs not yet negated)
     double o[10];
