@@ -1233,6 +1233,169 @@ int launch_zwalk_x2(const TileArgs& a0, const float* taps_host, int ntaps, cudaS
   return check_launch("xcorr_zwalk_x2");
 }
 
+// Persistent 2-D variant of xcorr_pair_f32 for large kernels (config 4): a
+// CTA walks output tiles; the next tile's input values are loaded from
+// global memory into registers (PF per thread) before the current tile's
+// FMAs, so the global-load latency of the staging is hidden behind compute;
+// after the tile they are written to the E/O pair copies.  Same arithmetic
+// as xcorr_pair_f32.
+constexpr int kPfRows = 12, kPfCols = 4;  // staged (row, column) slots per thread the register prefetch covers
+constexpr int kPairPF = kPfRows * kPfCols;
+
+template <int NW>
+__global__ void __launch_bounds__(256, 2) xcorr_pair_f32_pf(const TileArgs a, const __grid_constant__ TapsPairParam taps,
+                                                           int tiles_x, int tiles_y) {
+  extern __shared__ __align__(16) unsigned char smem_pf[];
+  constexpr int WIN = kPairVX + NW - 1;
+  constexpr int WLD = (WIN + 1) / 2;
+  const int tid = threadIdx.x;
+  const int tx = tid % a.txn, ty = tid / a.txn;
+  const int BX = a.txn * kPairVX, BY = a.tyn * 2;
+  const int ny = a.ny;
+  const int SY = a.sy, SXp = a.sx;
+  const int SXl = BX - kPairVX + 2 * WLD;
+  const int PE = (SY + 1) / 2;
+  float2* cE = reinterpret_cast<float2*>(smem_pf);
+  float2* cO = cE + (size_t)PE * SXp;
+  float* fE = reinterpret_cast<float*>(cE);
+  float* fO = reinterpret_cast<float*>(cO);
+  const int lane = tid & 31, nwarps = blockDim.x >> 5;
+  const int64_t n_tiles = a.batch * tiles_y * tiles_x;
+  float pf[kPairPF];
+
+  // staged element (r, c) of this thread: r = warp + 8 i (i < kPfRows), c = lane + 32 j (j < kPfCols)
+  auto fetch = [&](int64_t t) {  // global -> registers for tile t
+    const int64_t b = t / (tiles_x * tiles_y);
+    const int tt = (int)(t - b * tiles_x * tiles_y);
+    const int x0 = (tt % tiles_x) * BX, y0 = (tt / tiles_x) * BY;
+    const float* sp = reinterpret_cast<const float*>(a.s) + b * (int64_t)a.my * a.mx;
+    const int iy0 = y0 - a.py, ix0 = x0 - a.px;
+#pragma unroll
+    for (int i = 0; i < kPfRows; ++i) {
+      const int r = (tid >> 5) + i * nwarps;
+      int gy = iy0 + r;
+      const bool row_in = (unsigned)gy < (unsigned)a.my;
+      if (!row_in && a.boundary == CT_REPLICATE) gy = gy < 0 ? 0 : a.my - 1;
+      const float* srow = sp + (int64_t)gy * a.mx;
+#pragma unroll
+      for (int j = 0; j < kPfCols; ++j) {
+        const int c = lane + 32 * j;
+        int gx = ix0 + c;
+        float v = 0.f;
+        if (r < SY && c < SXl) {
+          if (row_in && (unsigned)gx < (unsigned)a.mx) {
+            v = __ldg(srow + gx);
+          } else if (a.boundary == CT_REPLICATE) {
+            gx = min(max(gx, 0), a.mx - 1);
+            v = __ldg(srow + gx);
+          }
+        }
+        pf[i * kPfCols + j] = v;
+      }
+    }
+  };
+  auto store = [&]() {  // registers -> E/O pair copies
+#pragma unroll
+    for (int i = 0; i < kPfRows; ++i) {
+      const int r = (tid >> 5) + i * nwarps;
+      if (r >= SY) break;
+      float* dE = fE + (size_t)(r >> 1) * SXp * 2 + (r & 1);
+      float* dO = r >= 1 ? fO + (size_t)((r - 1) >> 1) * SXp * 2 + ((r - 1) & 1) : nullptr;
+#pragma unroll
+      for (int j = 0; j < kPfCols; ++j) {
+        const int c = lane + 32 * j;
+        if (c < SXl) {
+          const float v = pf[i * kPfCols + j];
+          const int cp = pair_pad(c) * 2;
+          dE[cp] = v;
+          if (dO) dO[cp] = v;
+        }
+      }
+    }
+    if (SY & 1) {
+      for (int c = tid; c < SXp; c += blockDim.x) fE[(((SY - 1) >> 1) * SXp + c) * 2 + 1] = 0.f;
+    } else {
+      for (int c = tid; c < SXp; c += blockDim.x) fO[(((SY - 2) >> 1) * SXp + c) * 2 + 1] = 0.f;
+    }
+  };
+
+  int64_t t = blockIdx.x;
+  if (t < n_tiles) fetch(t);
+  for (; t < n_tiles; t += gridDim.x) {
+    __syncthreads();  // previous tile's compute done with E/O
+    store();
+    __syncthreads();
+    if (t + gridDim.x < n_tiles) fetch(t + gridDim.x);  // in flight during this tile's FMAs
+
+    const int64_t b = t / (tiles_x * tiles_y);
+    const int tt = (int)(t - b * tiles_x * tiles_y);
+    const int x0 = (tt % tiles_x) * BX, y0 = (tt / tiles_x) * BY;
+    float2 acc[kPairVX];
+#pragma unroll
+    for (int m = 0; m < kPairVX; ++m) acc[m] = make_float2(0.f, 0.f);
+    for (int j1 = 0; j1 < ny; ++j1) {
+      const int lr = 2 * ty + j1;
+      const float2* prow = ((lr & 1) ? cO : cE) + (size_t)(lr >> 1) * SXp;
+      float2 w[2 * WLD];
+#pragma unroll
+      for (int c = 0; c < WLD; ++c) {
+        const float4 q = *reinterpret_cast<const float4*>(prow + 10 * tx + 2 * c + 2 * (c >> 2));
+        w[2 * c] = make_float2(q.x, q.y);
+        w[2 * c + 1] = make_float2(q.z, q.w);
+      }
+      const float2* kr = taps.v + j1 * NW;
+#pragma unroll
+      for (int j2 = 0; j2 < NW; ++j2) {
+        const float2 kk = kr[j2];
+#pragma unroll
+        for (int m = 0; m < kPairVX; ++m) acc[m] = ffma2(kk, w[m + j2], acc[m]);
+      }
+    }
+    float* out = reinterpret_cast<float*>(a.out) + b * (int64_t)a.oy * a.ox;
+    const int y = y0 + 2 * ty;
+    const int x = x0 + tx * kPairVX;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (y + h >= a.oy) break;
+      float* orow = out + ((int64_t)y + h) * a.ox;
+#pragma unroll
+      for (int m = 0; m < kPairVX; ++m)
+        if (x + m < a.ox) orow[x + m] = h ? acc[m].y : acc[m].x;
+    }
+  }
+}
+
+template <int NW>
+int launch_pair_f32_pf(const TileArgs& a0, const float* taps_host, int ntaps, cudaStream_t st) {
+  TileArgs a = a0;
+  TapsPairParam taps;
+  for (int i = 0; i < ntaps; ++i) taps.v[i] = make_float2(taps_host[i], taps_host[i]);
+  const int BX = a.txn * kPairVX, BY = a.tyn * 2;
+  constexpr int WIN = kPairVX + NW - 1;
+  constexpr int WLD = (WIN + 1) / 2;
+  a.sy = BY + a.ny - 1;
+  const int sxl = BX - kPairVX + 2 * WLD;
+  a.sx = pair_pad(sxl - 1) + 1;
+  a.sx += (a.sx & 1);
+  const int nthr = a.txn * a.tyn;
+  CT_REQUIRE(nthr % 32 == 0 && nthr <= 256, "pair pf tile");
+  if (cdiv(a.sy, nthr / 32) > kPfRows || cdiv(sxl, 32) > kPfCols) {
+    set_error("pair pf tile too large for the register prefetch");
+    return CT_EUNSUPPORTED;
+  }
+  const int PE = (a.sy + 1) / 2, PO = a.sy / 2;
+  const size_t smem = (size_t)(PE + PO) * a.sx * sizeof(float2);
+  auto kern = xcorr_pair_f32_pf<NW>;
+  CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 1;
+  CT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nthr, smem));
+  const int tiles_x = (int)cdiv(a.ox, BX), tiles_y = (int)cdiv(a.oy, BY);
+  const int64_t n_tiles = a.batch * tiles_x * tiles_y;
+  const int64_t grid = std::min<int64_t>(n_tiles, (int64_t)num_sms() * std::max(1, per_sm));
+  kern<<<(unsigned)grid, nthr, smem, st>>>(a, taps, tiles_x, tiles_y);
+  return check_launch("xcorr_pair_f32_pf");
+}
+
 // Tile shape (threads along x, thread rows) minimising padded FMAs plus
 // staging over the whole output, for vx outputs per thread along x and
 // rows_per_thread output rows per thread.
@@ -1321,6 +1484,16 @@ int launch_variant(TileArgs a, int kind, int nw, bool is3d, int txn, int tyn, co
     return CT_EUNSUPPORTED;
   }
   if constexpr (sizeof(T) == 4) {
+    if (kind == 6 && !is3d) {
+      a.tiles_z = 1;
+      switch (nw) {
+#define CT_CASE(W) case W: return launch_pair_f32_pf<W>(a, reinterpret_cast<const float*>(taps), ntaps, st);
+        CT_CASE(7) CT_CASE(8) CT_CASE(9) CT_CASE(11) CT_CASE(15) CT_CASE(31)
+#undef CT_CASE
+      }
+      set_error("unsupported kernel width %d", nw);
+      return CT_EUNSUPPORTED;
+    }
     if (kind == 5) {  // z-walking 3-D kernel with packed FFMA2 (fp32)
       const int n = a.nz;
       const float* tf = reinterpret_cast<const float*>(taps);
@@ -1404,6 +1577,9 @@ int run_tiled_autotuned(TileArgs a, int nw, bool is3d, const T* taps, int ntaps,
     cands.push_back({1, tx, ty});
     for (Variant v : {Variant{1, 8, 32}, Variant{1, 16, 16}, Variant{1, 16, 8}, Variant{1, 8, 16}, Variant{1, 32, 8}})
       cands.push_back(v);
+    if (!is3d && nw >= 7 && (nw <= 9 || nw == 11 || nw == 15 || nw == 31))  // large 2-D kernels: persistent prefetch
+      for (Variant v : {Variant{6, 8, 32}, Variant{6, 16, 16}, Variant{6, 8, 16}, Variant{6, 16, 8}})
+        cands.push_back(v);
   }
   choose_tile(a, nw, VX, 4, &tx, &ty, false);
   cands.push_back({0, tx, ty});

@@ -442,13 +442,19 @@ inline unsigned finalize_grid(int64_t n_sys) { return (unsigned)std::min<int64_t
 // 32 rows for f32 (3 x 34 KB): per-pair reduction overhead is amortised over
 // more pixels, which matters for the cheaper FP32 math (measured: 16 rows with
 // a 6-deep ring is 25% slower than 32 rows with 3 buffers).
+#ifndef CT_MOM_BR32
+#define CT_MOM_BR32 32
+#endif
+#ifndef CT_MOM_NB32
+#define CT_MOM_NB32 3
+#endif
 template <typename T>
 constexpr int band_rows() {
-  return sizeof(T) == 8 ? 16 : 32;
+  return sizeof(T) == 8 ? 16 : CT_MOM_BR32;
 }
 template <typename T>
 constexpr int ring_buffers() {
-  return 3;
+  return sizeof(T) == 8 ? 3 : CT_MOM_NB32;
 }
 
 struct Plan {

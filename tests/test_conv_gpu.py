@@ -205,7 +205,7 @@ def test_large_batch_fullsize_roundtrip_property():
     assert np.array_equal(oa[i].cpu().numpy(), O.direct(a[i].cpu().numpy(), k, "full"))
 
 
-@pytest.mark.parametrize("kind", ["0", "1", "2"])
+@pytest.mark.parametrize("kind", ["0", "1", "2", "6"])
 def test_each_kernel_variant_matches_oracle(kind, monkeypatch):
     """Pin each tiled variant (0 register-tiled, 1 fp32 row-pair FFMA2, 2 TMA-staged
     persistent) and compare with the oracle: fp64 bit-exact, fp32 within 1e-5."""
