@@ -276,7 +276,9 @@ def secondary_configs(quick: bool):
     out["cfg1_conv2d_fp64_5x5"] = {"gpix_s": B * 260 * 260 / t / 1e9, "batch": B, "ms_per_launch": t * 1e3,
                                    "roofline": {"bound": "hbm", "achieved": bytes_ / t / 1e9, "peak": hbm,
                                                 "unit": "GB/s", "frac": bytes_ / t / 1e9 / hbm}}
-    del s, o
+    s1, o1 = s[:1].contiguous(), o[:1].contiguous()
+    out["cfg1_conv2d_fp64_5x5"]["single_call_ms"] = timeit(lambda: ct.direct_batch(s1, k, out=o1), 50) * 1e3
+    del s, o, s1, o1
     # cfg3: 3-D FULL fp32 128^3 * 7^3
     B3 = 8
     s3 = torch.rand((B3, 128, 128, 128), dtype=torch.float32, device="cuda")
@@ -288,7 +290,9 @@ def secondary_configs(quick: bool):
                                    "roofline": {"bound": "fp32", "achieved": fl / t / 1e12, "peak": 69.3,
                                                 "unit": "TFLOP/s", "frac": fl / t / 1e12 / 69.3,
                                                 "peak_note": "FFMA-chain microbenchmark on the box (tools/fp_peak.cu)"}}
-    del s3, o3
+    s1, o1 = s3[:1].contiguous(), o3[:1].contiguous()
+    out["cfg3_conv3d_fp32_7^3"]["single_call_ms"] = timeit(lambda: ct.direct_batch(s1, k3, out=o1), 20) * 1e3
+    del s3, o3, s1, o1
     # cfg4: large-kernel 2-D FULL fp32 2048^2 * 31^2
     B4 = 2
     s4 = torch.rand((B4, 2048, 2048), dtype=torch.float32, device="cuda")
@@ -300,7 +304,9 @@ def secondary_configs(quick: bool):
                                      "roofline": {"bound": "fp32", "achieved": fl / t / 1e12, "peak": 69.3,
                                                   "unit": "TFLOP/s", "frac": fl / t / 1e12 / 69.3,
                                                   "peak_note": "FFMA-chain microbenchmark on the box (tools/fp_peak.cu)"}}
-    del s4, o4
+    s1, o1 = s4[:1].contiguous(), o4[:1].contiguous()
+    out["cfg4_conv2d_fp32_31x31"]["single_call_ms"] = timeit(lambda: ct.direct_batch(s1, k4, out=o1), 10) * 1e3
+    del s4, o4, s1, o1
     # cfg5: multiscale fp32 1080x1920, max_level=3 (reduced stream: 2 videos x 64 frames in quick mode)
     nv, nf = (1, 64) if quick else (2, 128)
     fr = torch.empty((nv, nf, 1080, 1920), dtype=torch.float32, device="cuda")
