@@ -1049,149 +1049,169 @@ int launch_pair_f32(const TileArgs& a0, const float* taps_host, int ntaps, cudaS
   return check_launch("xcorr_pair_f32");
 }
 
-// fp32 z-walking kernel with packed FFMA2: the accumulators are (x, x+1)
-// float2 pairs and the taps (k, k) pairs in the parameter bank, so one
-// FFMA2 does two output FMAs.  A row's window pairs (v[j2+x], v[j2+x+1]) are
-// 8-byte aligned in the staged slice for one parity of j2 and in a copy of
-// the slice shifted by one element for the other (built in shared memory
-// after each TMA lands), so every operand is a single 64-bit load.
-template <int NZ, int NH, int NW, int TY, int ODD, int MAXT>
+// fp32 z-walking kernel with packed FFMA2 (same schedule as xcorr_zwalk:
+// persistent runs of output slices, 3-stage TMA slice ring, NZ register
+// slots).  The accumulators are (x, x+1) float2 pairs and the taps (k, k)
+// pairs in the parameter bank (padded to 16 bytes per kernel row), so one
+// FFMA2 does two output FMAs.  A window row is loaded as 16-byte vectors
+// from the aligned base below it (SH4 = its offset, compile-time); the
+// operand pairs (v[e], v[e+1]) are register pairs, odd ones built by moves.
+template <int NZ, int NH, int NW, int TY, int SH4, int MAXT>
 __global__ void __launch_bounds__(MAXT, 1) xcorr_zwalk_x2(const TileArgs a, const __grid_constant__ TapsPairParam taps,
-                                                         const __grid_constant__ CUtensorMap tmap, int pxa, int zc) {
+                                                         const __grid_constant__ CUtensorMap tmap, int pxa,
+                                                         int64_t per_cta) {
   extern __shared__ __align__(128) unsigned char smem_zw2[];
   constexpr int NS = 3;
   constexpr int VX = 4;
-  constexpr int NPE = (VX + NW - 1 + 1) / 2;  // aligned pairs per window row
-  constexpr int NPO = (VX + NW - 2) / 2;      // shifted pairs per window row
+  constexpr int NV4 = (SH4 + VX + NW - 1 + 3) / 4;  // 16-byte loads per window row
+  constexpr int KP = (NW + 1) / 2 * 2;             // (k,k) pairs per kernel row, 16-byte padded
   const int tid = threadIdx.x;
-  const int nthr = blockDim.x;
   const int tx = tid % a.txn, ty = tid / a.txn;
   const int BX = a.txn * VX, BY = a.tyn * TY;
-  const int x0 = blockIdx.x * BX, y0 = blockIdx.y * BY;
+  const int tiles_x = (a.ox + BX - 1) / BX, tiles_y = (a.oy + BY - 1) / BY;
   const int sh = pxa - a.px;
-  const int plane = a.sx * a.sy;
-  const size_t stage_bytes = ((size_t)plane * sizeof(float) + 127) & ~size_t(127);
+  const size_t stage_bytes = ((size_t)a.sx * a.sy * sizeof(float) + 127) & ~size_t(127);
   auto stage = [&](int s) { return reinterpret_cast<float*>(smem_zw2 + (size_t)s * stage_bytes); };
-  float* shifted = reinterpret_cast<float*>(smem_zw2 + NS * stage_bytes);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_zw2 + (NS + 1) * stage_bytes);
-  const uint32_t box_bytes = (uint32_t)(plane * sizeof(float));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_zw2 + NS * stage_bytes);
+  const uint32_t box_bytes = (uint32_t)(a.sx * a.sy * sizeof(float));
   const bool active = ty < a.tyn;
-  const int b = (int)(blockIdx.z / a.tiles_z);
-  const int z0 = (int)(blockIdx.z % a.tiles_z) * zc;
-  const int z1 = min(z0 + zc, a.oz);
-  const int s_beg = z0 - a.pz, s_end = z1 - a.pz + NZ - 1;
-  const int g_lo = max(0, s_beg), g_hi = min(a.mz, s_end);
-  const int nsl = max(0, g_hi - g_lo);
+  const int64_t total = a.batch * tiles_y * tiles_x * (int64_t)a.oz;
+  int64_t pos = (int64_t)blockIdx.x * per_cta;
+  const int64_t end = min(total, pos + per_cta);
   if (tid == 0) {
     for (int i = 0; i < NS; ++i) mbar_init(&bars[i], 1);
     mbar_fence_init();
   }
   __syncthreads();
-  auto issue = [&](int k) {
-    if (tid == 0) {
-      fence_proxy_async_smem();
-      mbar_arrive_expect_tx(&bars[k % NS], box_bytes);
-      tma_load_4d(stage(k % NS), &tmap, &bars[k % NS], x0 - pxa, y0 - a.py, g_lo + k, b);
-    }
-  };
-  for (int k = 0; k < NS && k < nsl; ++k) issue(k);
+  int gcount = 0;
+  // aligned window base of this thread within a staged row (sh + tx*VX - SH4)
+  const int wb = (ty * TY) * a.sx + sh + tx * VX - SH4;
 
-  float2 acc[NZ][TY][VX / 2];
-#pragma unroll
-  for (int j = 0; j < NZ; ++j)
-#pragma unroll
-    for (int yi = 0; yi < TY; ++yi)
-#pragma unroll
-      for (int x = 0; x < VX / 2; ++x) acc[j][yi][x] = make_float2(0.f, 0.f);
+  while (pos < end) {
+    const int64_t col = pos / a.oz;
+    const int z0 = (int)(pos - col * a.oz);
+    const int64_t left = end - pos;
+    const int z1 = left < (int64_t)(a.oz - z0) ? z0 + (int)left : a.oz;
+    pos += z1 - z0;
+    const int b = (int)(col / (tiles_x * tiles_y));
+    const int tt = (int)(col - (int64_t)b * tiles_x * tiles_y);
+    const int x0 = (tt % tiles_x) * BX, y0 = (tt / tiles_x) * BY;
+    const int s_beg = z0 - a.pz, s_end = z1 - a.pz + NZ - 1;
+    const int g_lo = max(0, s_beg), g_hi = min(a.mz, s_end);
+    const int nsl = max(0, g_hi - g_lo);
+    const int g0 = gcount;
+    auto issue = [&](int k) {
+      if (tid == 0) {
+        const int st = (g0 + k) % NS;
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&bars[st], box_bytes);
+        tma_load_4d(stage(st), &tmap, &bars[st], x0 - pxa, y0 - a.py, g_lo + k, b);
+      }
+    };
+    for (int k = 0; k < NS && k < nsl; ++k) issue(k);
 
-  float* out = reinterpret_cast<float*>(a.out) + (int64_t)b * a.oz * a.oy * a.ox;
-  const int ox = x0 + tx * VX;
-  // window base element of this thread; ODD = base parity (sh parity)
-  const int wb = (ty * TY) * a.sx + sh + tx * VX;
-  for (int s = s_beg; s < s_end; ++s) {
-    if (s >= g_lo && s < g_hi) {
-      const int k = s - g_lo;
-      mbar_wait(&bars[k % NS], (uint32_t)((k / NS) & 1));
-      const float* tile = stage(k % NS);
-      for (int i = tid; i < plane - 1; i += nthr) shifted[i] = tile[i + 1];
-      __syncthreads();
-      const int jlo = max(0, s + a.pz - z1 + 1), jhi = min(NZ - 1, s + a.pz - z0);
-      if (active) {
-        // pairs starting at window offset 2m (E) and 2m+1 (O)
-        const float* srcE = ODD ? shifted + wb - 1 : tile + wb;
-        const float* srcO = ODD ? tile + wb + 1 : shifted + wb;
-#pragma unroll 1
-        for (int j1 = 0; j1 < NH; ++j1) {
-          float2 pe[TY][NPE], po[TY][NPO > 0 ? NPO : 1];
+    float2 acc[NZ][TY][VX / 2];
 #pragma unroll
-          for (int yi = 0; yi < TY; ++yi) {
-            const int ro = (yi + j1) * a.sx;
-#pragma unroll
-            for (int m = 0; m < NPE; ++m) pe[yi][m] = *reinterpret_cast<const float2*>(srcE + ro + 2 * m);
-#pragma unroll
-            for (int m = 0; m < NPO; ++m) po[yi][m] = *reinterpret_cast<const float2*>(srcO + ro + 2 * m);
-          }
-          const float2* kj1 = taps.v + j1 * NW;
-          auto plane = [&](int j) {
-            const float2* kr = kj1 + j * NH * NW;
-#pragma unroll
-            for (int j2 = 0; j2 < NW; ++j2) {
-              const float2 kk = kr[j2];
-#pragma unroll
-              for (int yi = 0; yi < TY; ++yi)
-#pragma unroll
-                for (int xp = 0; xp < VX / 2; ++xp) {
-                  const int e = 2 * xp + j2;  // window offset of the pair
-                  const float2 w = (e & 1) ? po[yi][e >> 1] : pe[yi][e >> 1];
-                  acc[j][yi][xp] = ffma2(kk, w, acc[j][yi][xp]);
-                }
-            }
-          };
-          if (jlo == 0 && jhi == NZ - 1) {  // interior slice: branch-free, all slots interleavable
-#pragma unroll
-            for (int j = 0; j < NZ; ++j) plane(j);
-          } else {
-#pragma unroll
-            for (int j = 0; j < NZ; ++j)
-              if (j >= jlo && j <= jhi) plane(j);
-          }
-        }
-      }
-      __syncthreads();  // stage and shifted copy consumed
-      if (k + NS < nsl) issue(k + NS);
-    }
-    const int zo = s + a.pz - (NZ - 1);
-    if (zo >= z0 && zo < z1 && active) {
-#pragma unroll
-      for (int yi = 0; yi < TY; ++yi) {
-        const int y = y0 + ty * TY + yi;
-        if (y >= a.oy) break;
-        float* orow = out + ((int64_t)zo * a.oy + y) * a.ox;
-#pragma unroll
-        for (int xp = 0; xp < VX / 2; ++xp) {
-          if (ox + 2 * xp < a.ox) orow[ox + 2 * xp] = acc[NZ - 1][yi][xp].x;
-          if (ox + 2 * xp + 1 < a.ox) orow[ox + 2 * xp + 1] = acc[NZ - 1][yi][xp].y;
-        }
-      }
-    }
-#pragma unroll
-    for (int j = NZ - 1; j > 0; --j)
+    for (int j = 0; j < NZ; ++j)
 #pragma unroll
       for (int yi = 0; yi < TY; ++yi)
 #pragma unroll
-        for (int x = 0; x < VX / 2; ++x) acc[j][yi][x] = acc[j - 1][yi][x];
+        for (int x = 0; x < VX / 2; ++x) acc[j][yi][x] = make_float2(0.f, 0.f);
+
+    float* out = reinterpret_cast<float*>(a.out) + (int64_t)b * a.oz * a.oy * a.ox;
+    const int ox = x0 + tx * VX;
+    for (int s = s_beg; s < s_end; ++s) {
+      if (s >= g_lo && s < g_hi) {
+        const int k = s - g_lo;
+        const int g = g0 + k;
+        mbar_wait(&bars[g % NS], (uint32_t)((g / NS) & 1));
+        const int jlo = max(0, s + a.pz - z1 + 1), jhi = min(NZ - 1, s + a.pz - z0);
+        const float* tile = stage(g % NS) + wb;
+        if (active) {
+#pragma unroll 1
+          for (int j1 = 0; j1 < NH; ++j1) {
+            float v[TY][NV4 * 4];
 #pragma unroll
-    for (int yi = 0; yi < TY; ++yi)
+            for (int yi = 0; yi < TY; ++yi) {
+              const float4* rp = reinterpret_cast<const float4*>(tile + (yi + j1) * a.sx);
 #pragma unroll
-      for (int x = 0; x < VX / 2; ++x) acc[0][yi][x] = make_float2(0.f, 0.f);
+              for (int c = 0; c < NV4; ++c) {
+                const float4 q = rp[c];
+                v[yi][4 * c] = q.x;
+                v[yi][4 * c + 1] = q.y;
+                v[yi][4 * c + 2] = q.z;
+                v[yi][4 * c + 3] = q.w;
+              }
+            }
+            const float2* kj1 = taps.v + j1 * KP;
+            auto plane = [&](int j) {
+              const float2* kr = kj1 + j * NH * KP;
+#pragma unroll
+              for (int j2 = 0; j2 < NW; ++j2) {
+                const float2 kk = kr[j2];
+#pragma unroll
+                for (int yi = 0; yi < TY; ++yi)
+#pragma unroll
+                  for (int xp = 0; xp < VX / 2; ++xp) {
+                    const int e = SH4 + 2 * xp + j2;
+                    acc[j][yi][xp] = ffma2(kk, make_float2(v[yi][e], v[yi][e + 1]), acc[j][yi][xp]);
+                  }
+              }
+            };
+            if (jlo == 0 && jhi == NZ - 1) {
+#pragma unroll
+              for (int j = 0; j < NZ; ++j) plane(j);
+            } else {
+#pragma unroll
+              for (int j = 0; j < NZ; ++j)
+                if (j >= jlo && j <= jhi) plane(j);
+            }
+          }
+        }
+        __syncthreads();  // stage consumed
+        if (k + NS < nsl) issue(k + NS);
+      }
+      const int zo = s + a.pz - (NZ - 1);
+      if (zo >= z0 && zo < z1 && active) {
+#pragma unroll
+        for (int yi = 0; yi < TY; ++yi) {
+          const int y = y0 + ty * TY + yi;
+          if (y >= a.oy) break;
+          float* orow = out + ((int64_t)zo * a.oy + y) * a.ox;
+#pragma unroll
+          for (int xp = 0; xp < VX / 2; ++xp) {
+            if (ox + 2 * xp < a.ox) orow[ox + 2 * xp] = acc[NZ - 1][yi][xp].x;
+            if (ox + 2 * xp + 1 < a.ox) orow[ox + 2 * xp + 1] = acc[NZ - 1][yi][xp].y;
+          }
+        }
+      }
+#pragma unroll
+      for (int j = NZ - 1; j > 0; --j)
+#pragma unroll
+        for (int yi = 0; yi < TY; ++yi)
+#pragma unroll
+          for (int x = 0; x < VX / 2; ++x) acc[j][yi][x] = acc[j - 1][yi][x];
+#pragma unroll
+      for (int yi = 0; yi < TY; ++yi)
+#pragma unroll
+        for (int x = 0; x < VX / 2; ++x) acc[0][yi][x] = make_float2(0.f, 0.f);
+    }
+    gcount += nsl;
   }
 }
 
 template <int NZ, int NH, int NW, int TY, int MAXT = 256>
 int launch_zwalk_x2(const TileArgs& a0, const float* taps_host, int ntaps, cudaStream_t st) {
   TileArgs a = a0;
+  constexpr int KP = (NW + 1) / 2 * 2;
+  static_assert(NZ * NH * KP <= MaxTaps<float>::value, "padded taps exceed the parameter block");
   TapsPairParam taps;
-  for (int i = 0; i < ntaps; ++i) taps.v[i] = make_float2(taps_host[i], taps_host[i]);
+  for (int r = 0; r < NZ * NH; ++r)
+    for (int j2 = 0; j2 < KP; ++j2) {
+      const float kv = j2 < NW ? taps_host[r * NW + j2] : 0.f;
+      taps.v[r * KP + j2] = make_float2(kv, kv);
+    }
+  (void)ntaps;
   constexpr int VX = 4;
   if (a.txn <= 0 || a.tyn <= 0 || a.txn * a.tyn > MAXT) choose_zwalk_tile(a.oy, a.ox, VX, TY, NH, NW, &a.txn, &a.tyn, MAXT);
   if (getenv("CT_ZW_TXN") && getenv("CT_ZW_TYN")) {  // probing only
@@ -1199,27 +1219,30 @@ int launch_zwalk_x2(const TileArgs& a0, const float* taps_host, int ntaps, cudaS
     a.tyn = atoi(getenv("CT_ZW_TYN"));
   }
   const int pxa = (a.px + 3) / 4 * 4;
-  const int sh = pxa - a.px;
+  const int sh = pxa - a.px;  // 0..3
   const int BX = a.txn * VX, BY = a.tyn * TY;
-  a.sx = (sh + BX + NW - 1 + 1 + 3) / 4 * 4;  // +1: the shifted copy's last pair
+  const int nv4 = (sh + VX + NW - 1 + 3) / 4;
+  a.sx = std::max((sh + BX + NW - 1 + 3) / 4 * 4, BX - VX + 4 * nv4);  // every thread's vector loads stay in the row
   a.sy = BY + NH - 1;
   const size_t stage_bytes = ((size_t)a.sx * a.sy * sizeof(float) + 127) & ~size_t(127);
-  const size_t smem = 4 * stage_bytes + 64;
+  const size_t smem = 3 * stage_bytes + 64;
   CT_REQUIRE(smem <= 227 * 1024, "zwalk tile too large");
   const int nthr = (int)cdiv(a.txn * a.tyn, 32) * 32;
-  void (*kern)(const TileArgs, const TapsPairParam, const CUtensorMap, int, int);
-  if (sh & 1)
-    kern = xcorr_zwalk_x2<NZ, NH, NW, TY, 1, MAXT>;
-  else
-    kern = xcorr_zwalk_x2<NZ, NH, NW, TY, 0, MAXT>;
+  void (*kern)(const TileArgs, const TapsPairParam, const CUtensorMap, int, int64_t);
+  switch (sh) {
+    case 0: kern = xcorr_zwalk_x2<NZ, NH, NW, TY, 0, MAXT>; break;
+    case 1: kern = xcorr_zwalk_x2<NZ, NH, NW, TY, 1, MAXT>; break;
+    case 2: kern = xcorr_zwalk_x2<NZ, NH, NW, TY, 2, MAXT>; break;
+    default: kern = xcorr_zwalk_x2<NZ, NH, NW, TY, 3, MAXT>; break;
+  }
   CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 1;
   CT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nthr, smem));
-  const int64_t plane_ctas = cdiv(a.ox, BX) * cdiv(a.oy, BY) * a.batch;
-  int zc = zwalk_chunk(a.oz, NZ, plane_ctas, per_sm);
-  if (const char* e = getenv("CT_ZW_ZC")) zc = std::max(1, atoi(e));  // probing only
-  a.tiles_z = (int)cdiv(a.oz, zc);
-  CT_REQUIRE(a.batch * a.tiles_z <= 65535, "too many z chunks");
+  const int64_t total = cdiv(a.ox, BX) * cdiv(a.oy, BY) * a.batch * a.oz;
+  const int64_t slots = (int64_t)num_sms() * std::max(1, per_sm);
+  int64_t per_cta = std::max<int64_t>(cdiv(total, slots), 2 * NZ);
+  if (const char* e = getenv("CT_ZW_ZC")) per_cta = std::max(1, atoi(e));  // probing only
+  const int64_t nctas = cdiv(total, per_cta);
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof(tmap));
   if (a.sx > 256 || a.sy > 256 ||
@@ -1228,8 +1251,10 @@ int launch_zwalk_x2(const TileArgs& a0, const float* taps_host, int ntaps, cudaS
     set_error("tensor map encode failed");
     return CT_EUNSUPPORTED;
   }
-  dim3 grid((unsigned)cdiv(a.ox, BX), (unsigned)cdiv(a.oy, BY), (unsigned)(a.batch * a.tiles_z));
-  kern<<<grid, nthr, smem, st>>>(a, taps, tmap, pxa, zc);
+  if (getenv("CT_DEBUG"))
+    fprintf(stderr, "xcorr_zwalk_x2 TY %d MAXT %d: tile %dx%d (%d thr) per_cta %lld per_sm %d ctas %lld\n", TY, MAXT,
+            BX, BY, nthr, (long long)per_cta, per_sm, (long long)nctas);
+  kern<<<(unsigned)nctas, nthr, smem, st>>>(a, taps, tmap, pxa, per_cta);
   return check_launch("xcorr_zwalk_x2");
 }
 
