@@ -39,14 +39,12 @@
 namespace ct {
 namespace {
 
-constexpr int kBoxCols = 256;        // frame columns per tile (TMA box inner extent)
-constexpr int kTileGridCols = 255;   // grid columns when the frame fits one tile (w <= 256)
+// BC = frame columns per tile (TMA box inner extent) = threads per CTA; a
+// frame that fits one tile uses BC-1 grid columns of it.
 // With several column tiles the stride is 252 grid columns: a TMA box must
 // start 16-byte aligned (a start at element 255 faults with an illegal
 // instruction), and 252 is a multiple of 4 f32 / 2 f64 elements.
-constexpr int kTileStrideMulti = 252;
-constexpr int kThreads = 256;        // one grid column per thread
-constexpr int kRedSeg = 16;          // reduction tree: 16 segments of 16 threads
+// (multi-tile stride: BC - 4 grid columns)
 #ifndef CT_MOM_PACKED_F32
 #define CT_MOM_PACKED_F32 1
 #endif
@@ -76,20 +74,21 @@ struct MomentArgs {
 // pyramid level never re-reads the full-size frame: band rows [gy0, gy0+BR)
 // and this tile's columns map to dec rows [gy0/2, (gy0+BR)/2) and dec columns
 // [cx0/2, (cx0 + tile_cols + 1)/2), disjoint across CTAs.
-template <typename T, int BR, int NT>
+template <typename T, int BR, int NT, int BC>
 __device__ __forceinline__ void write_dec(const MomentArgs& a, const T* buf, int64_t v, int f, int gy0, int cx0,
                                           int tid) {
-  static_assert(NT % 128 == 0, "write_dec maps 128 dec columns per thread row");
+  constexpr int DC = BC / 2;  // dec columns per tile (at most)
+  static_assert(NT % DC == 0, "write_dec maps DC dec columns per thread row");
   const int dy0 = gy0 >> 1, dx0 = cx0 >> 1;
   const int ndy = min(BR / 2, a.dh - dy0);
   const int ndx = min((a.tile_cols + 1) >> 1, a.dw - dx0);
-  const int xx = tid & 127;  // dec column of this thread (a tile has <= 128 of them)
+  const int xx = tid % DC;  // dec column of this thread
   if (ndy <= 0 || xx >= ndx) return;
   T* dst = reinterpret_cast<T*>(a.dec) + ((v * a.n_frames + f) * (int64_t)a.dh + dy0) * a.dw + dx0 + xx;
 #pragma unroll 4
-  for (int yy = tid >> 7; yy < ndy; yy += NT / 128) {
-    const T* p0 = buf + (2 * yy) * kBoxCols + 2 * xx;
-    const T* p1 = p0 + kBoxCols;
+  for (int yy = tid / DC; yy < ndy; yy += NT / DC) {
+    const T* p0 = buf + (2 * yy) * BC + 2 * xx;
+    const T* p1 = p0 + BC;
     T d;
     if constexpr (sizeof(T) == 8) {
       d = __dmul_rn(0.25, __dadd_rn(__dadd_rn(__dadd_rn(p0[0], p0[1]), p1[0]), p1[1]));
@@ -100,18 +99,19 @@ __device__ __forceinline__ void write_dec(const MomentArgs& a, const T* buf, int
   }
 }
 
-template <typename T, int BR, int NB>
+template <typename T, int BR, int NB, int BC>
 struct Smem {  // NB = frame-band buffers in the TMA ring (NB - 2 frames in flight per pair)
-  static constexpr size_t buf_elems = (size_t)(BR + 1) * kBoxCols + 8;  // +8: masked right-neighbour reads
+  static constexpr size_t buf_elems = (size_t)(BR + 1) * BC + 8;  // +8: masked right-neighbour reads
   static constexpr size_t buf_bytes = (buf_elems * sizeof(T) + 127) & ~size_t(127);
   // the reduction scratch lives in the dead previous-frame buffer; f32 bands
   // are smaller, so lane pairs are combined first (half the scratch)
-  static constexpr bool half_red = buf_bytes < 10 * kThreads * sizeof(double);
-  static constexpr int red_n = half_red ? kThreads / 2 : kThreads;
+  static constexpr bool half_red = buf_bytes < 10 * BC * sizeof(double);
+  static constexpr int red_n = half_red ? BC / 2 : BC;
+  static constexpr int seg = BC >= 256 ? 16 : 8;  // stage-1 segments per value (10 * seg <= BC threads)
   static_assert(buf_bytes >= 10 * (size_t)red_n * sizeof(double), "reduction scratch must fit a band buffer");
   static constexpr size_t bars_off = NB * buf_bytes;
   static constexpr size_t part_off = bars_off + 64;
-  static constexpr size_t total = part_off + 10 * kRedSeg * sizeof(double);
+  static constexpr size_t total = part_off + 10 * seg * sizeof(double);
 };
 
 // One thread's sweep down its column of the band for one frame pair (A, B):
@@ -128,7 +128,7 @@ struct Smem {  // NB = frame-band buffers in the TMA ring (NB - 2 frames in flig
 // four adds per row replace one multiply and four FMAs.  Rows outside
 // [r_beg, r_end] leave S unchanged (t_r = 0) but still advance Q and QQ.
 // CHECK=false is the interior fast path (all rows, no per-row tests).
-template <typename T, int BR, bool CHECK>
+template <typename T, int BR, bool CHECK, int BC>
 __device__ __forceinline__ void sweep(const T* __restrict__ A, const T* __restrict__ B, int col, int r_beg,
                                       int r_end, typename AccT<T>::type (&m)[10]) {
   using ACC = typename AccT<T>::type;
@@ -143,8 +143,8 @@ __device__ __forceinline__ void sweep(const T* __restrict__ A, const T* __restri
   }
 #pragma unroll
   for (int r = 1; r <= BR; ++r) {
-    const T* ra = A + r * kBoxCols + col;
-    const T* rb = B + r * kBoxCols + col;
+    const T* ra = A + r * BC + col;
+    const T* rb = B + r * BC + col;
     const ACC a0 = (ACC)ra[0], a1 = (ACC)ra[1], b0 = (ACC)rb[0], b1 = (ACC)rb[1];
     const ACC P0 = a0 + b0, P1 = a1 + b1, D0 = b0 - a0, D1 = b1 - a1;
     const ACC nhP = P0 + P1, ndP = P1 - P0, nsD = D0 + D1;
@@ -207,11 +207,11 @@ __device__ __forceinline__ float2 f2fma(float2 a, float2 b, float2 c) {
   return *reinterpret_cast<float2*>(&r);
 }
 
-template <int BR>
+template <int BR, int BC>
 __device__ __forceinline__ void sweep_x2(const float* __restrict__ A, const float* __restrict__ B, int col,
                                          float (&m)[10]) {
   constexpr int H = BR / 2;
-  auto ld = [&](const float* F, int r, int c) { return make_float2(F[r * kBoxCols + c], F[(r + H) * kBoxCols + c]); };
+  auto ld = [&](const float* F, int r, int c) { return make_float2(F[r * BC + c], F[(r + H) * BC + c]); };
   float2 s1 = {0, 0}, s2 = {0, 0}, s3 = {0, 0}, s4 = {0, 0}, s5 = {0, 0}, s6 = {0, 0};
   float2 q2, q3, q5, qq3, hP, dP, sD;
   {
@@ -267,11 +267,13 @@ __device__ __forceinline__ void sweep_x2(const float* __restrict__ A, const floa
   m[9] = u4x + fmaf(K * K, s3.y, fmaf(2 * K, u2y, u4y));
 }
 
-template <typename T, int BR, int NB>
-__global__ void __launch_bounds__(kThreads, 2) ttc_moments_kernel(const MomentArgs a,
+template <typename T, int BR, int NB, int BC>
+__global__ void __launch_bounds__(BC, 512 / BC) ttc_moments_kernel(const MomentArgs a,
                                                                   const __grid_constant__ CUtensorMap tmap) {
   using ACC = typename AccT<T>::type;
-  using S = Smem<T, BR, NB>;
+  using S = Smem<T, BR, NB, BC>;
+  constexpr int kThreads = BC;
+  constexpr int kRedSeg = S::seg;
   extern __shared__ __align__(128) unsigned char smem[];
   auto buf = [&](int k) { return reinterpret_cast<T*>(smem + (size_t)k * S::buf_bytes); };
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::bars_off);
@@ -288,7 +290,7 @@ __global__ void __launch_bounds__(kThreads, 2) ttc_moments_kernel(const MomentAr
   const int p1 = min(p0 + a.chunk, n_pairs);  // pairs [p0, p1) -> frames p0..p1
   if (p0 >= p1) return;
   const int nload = p1 - p0 + 1;
-  constexpr uint32_t kBoxBytes = (uint32_t)((BR + 1) * kBoxCols * sizeof(T));
+  constexpr uint32_t kBoxBytes = (uint32_t)((BR + 1) * BC * sizeof(T));
 
   const int gx = cx0 + tid;
   const bool in_col = tid < a.tile_cols && gx >= a.border && gx < a.gw - a.border;
@@ -311,8 +313,8 @@ __global__ void __launch_bounds__(kThreads, 2) ttc_moments_kernel(const MomentAr
     } else {
       const T* src = reinterpret_cast<const T*>(a.frames) + grow * a.w;
       const int64_t rows_left = a.n_videos * a.n_frames * (int64_t)a.h - grow;
-      for (int idx = tid; idx < (BR + 1) * kBoxCols; idx += kThreads) {
-        const int r = idx / kBoxCols, c = idx - r * kBoxCols;
+      for (int idx = tid; idx < (BR + 1) * BC; idx += kThreads) {
+        const int r = idx / BC, c = idx - r * BC;
         T val = T(0);
         if (r < rows_left && cx0 + c < a.w) val = src[(int64_t)r * a.w + cx0 + c];
         dst[idx] = val;
@@ -343,17 +345,17 @@ __global__ void __launch_bounds__(kThreads, 2) ttc_moments_kernel(const MomentAr
     const T* B = buf((i + 1) % NB);
 
     if (a.dec) {  // frames p0..p1-1 belong to this chunk (the last chunk also owns frame p1)
-      write_dec<T, BR, kThreads>(a, A, v, p, gy0, cx0, tid);
-      if (p1 == n_pairs && i == p1 - p0 - 1) write_dec<T, BR, kThreads>(a, B, v, p1, gy0, cx0, tid);
+      write_dec<T, BR, kThreads, BC>(a, A, v, p, gy0, cx0, tid);
+      if (p1 == n_pairs && i == p1 - p0 - 1) write_dec<T, BR, kThreads, BC>(a, B, v, p1, gy0, cx0, tid);
     }
     ACC m[10];
     if (r_beg <= 1 && r_end >= BR) {
       if constexpr (sizeof(T) == 4 && kPackedF32)
-        sweep_x2<BR>(A, B, tid, m);
+        sweep_x2<BR, BC>(A, B, tid, m);
       else
-        sweep<T, BR, false>(A, B, tid, 1, BR, m);
+        sweep<T, BR, false, BC>(A, B, tid, 1, BR, m);
     } else {
-      sweep<T, BR, true>(A, B, tid, r_beg, r_end, m);
+      sweep<T, BR, true, BC>(A, B, tid, r_beg, r_end, m);
     }
 
     // this thread's ten sums, order m00 m01 m02 m11 m12 m22 r0 r1 r2 et2 (rhs not yet negated)
@@ -461,19 +463,35 @@ struct Plan {
   int n_bands, n_ctiles, units, chunk, n_chunks, tile_cols;
 };
 
-template <typename T>
+// Tile width: 256 columns, or 128 (4 CTAs of 4 warps per SM instead of 2 of
+// 8, so the per-pair barriers of different CTAs overlap better) when the
+// frame needs several tiles anyway and 128-wide tiles load no more columns.
+// Measured on cfg5 (1080x1920 f32): 128 is 4.5% faster; on 256-wide frames
+// 256 (one tile) is much faster.
+inline int tile_loaded_cols(int gw, int bc) {
+  const int tc = gw <= bc - 1 ? bc - 1 : bc - 4;
+  return (gw + tc - 1) / tc * bc;
+}
+inline int pick_bc(int w) {
+  if (const char* e = getenv("CT_MOM_BC")) return atoi(e) == 128 ? 128 : 256;  // probing only
+  const int gw = w - 1;
+  if (gw <= 255) return 256;
+  return tile_loaded_cols(gw, 128) <= tile_loaded_cols(gw, 256) ? 128 : 256;
+}
+
+template <typename T, int BC>
 Plan make_plan(int64_t n_videos, int n_frames, int h, int w) {
   Plan p{};
   constexpr int BR = band_rows<T>();
   const int gh = h - 1, gw = w - 1;
   p.n_bands = (gh + BR - 1) / BR;
-  p.tile_cols = gw <= kTileGridCols ? kTileGridCols : kTileStrideMulti;
+  p.tile_cols = gw <= BC - 1 ? BC - 1 : BC - 4;
   p.n_ctiles = (gw + p.tile_cols - 1) / p.tile_cols;
   p.units = p.n_bands * p.n_ctiles;
   const int n_pairs = n_frames - 1;
   // ~4 waves of resident CTAs (2 per SM), but >= 8 pairs per CTA so the
   // one-frame time halo of each chunk stays small
-  const int64_t target = (int64_t)num_sms() * 2 * 4;
+  const int64_t target = (int64_t)num_sms() * (512 / BC) * 4;
   const int64_t per_chunk = std::max<int64_t>(1, (int64_t)p.units * n_videos);
   int64_t chunks = std::max<int64_t>(1, (target + per_chunk - 1) / per_chunk);
   chunks = std::min<int64_t>(chunks, std::max(1, n_pairs / 8));
@@ -484,19 +502,23 @@ Plan make_plan(int64_t n_videos, int n_frames, int h, int w) {
 }
 
 template <typename T>
+Plan make_plan(int64_t n_videos, int n_frames, int h, int w) {
+  return pick_bc(w) == 128 ? make_plan<T, 128>(n_videos, n_frames, h, w) : make_plan<T, 256>(n_videos, n_frames, h, w);
+}
+
+template <typename T>
 size_t ws_bytes(int64_t n_videos, int n_frames, int h, int w) {
   if (n_frames < 2 || h < 2 || w < 2) return 0;
   const Plan p = make_plan<T>(n_videos, n_frames, h, w);
   return (size_t)n_videos * (n_frames - 1) * p.units * 10 * sizeof(double);
 }
 
-template <typename T>
-int launch(const T* frames, int64_t n_videos, int n_frames, int h, int w, int border, double* sums, void* ws,
-           size_t ws_size, void* dec, cudaStream_t st) {
+template <typename T, int BC>
+int launch_bc(const T* frames, int64_t n_videos, int n_frames, int h, int w, int border, double* sums, void* ws,
+              size_t ws_size, void* dec, cudaStream_t st) {
   const int n_pairs = n_frames - 1;
-  if (n_pairs <= 0 || n_videos == 0) return CT_OK;
   constexpr int BR = band_rows<T>();
-  const Plan p = make_plan<T>(n_videos, n_frames, h, w);
+  const Plan p = make_plan<T, BC>(n_videos, n_frames, h, w);
   const size_t need = ws_bytes<T>(n_videos, n_frames, h, w);
   CT_REQUIRE(ws != nullptr && ws_size >= need, "moments workspace too small (%zu < %zu)", ws_size, need);
   CT_REQUIRE(n_videos <= 65535 && p.n_chunks <= 65535, "too many videos/chunks for one launch");
@@ -521,19 +543,27 @@ int launch(const T* frames, int64_t n_videos, int n_frames, int h, int w, int bo
   memset(&tmap, 0, sizeof(tmap));
   static const bool no_tma = getenv("CT_NO_TMA") != nullptr;  // debugging switch: force the LDG loader
   a.use_tma = !no_tma && encode_tmap_2d(&tmap, frames, sizeof(T), (uint64_t)w,
-                                        (uint64_t)(n_videos * n_frames * (int64_t)h), kBoxCols, BR + 1);
+                                        (uint64_t)(n_videos * n_frames * (int64_t)h), BC, BR + 1);
   constexpr int NB = ring_buffers<T>();
-  using S = Smem<T, BR, NB>;
-  auto kern = ttc_moments_kernel<T, BR, NB>;
+  using S = Smem<T, BR, NB, BC>;
+  auto kern = ttc_moments_kernel<T, BR, NB, BC>;
   CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::total));
   dim3 grid((unsigned)p.units, (unsigned)p.n_chunks, (unsigned)n_videos);
-  kern<<<grid, kThreads, S::total, st>>>(a, tmap);
+  kern<<<grid, BC, S::total, st>>>(a, tmap);
   int rc = check_launch("ttc_moments");
   if (rc) return rc;
   const int64_t n_sys = n_videos * n_pairs;
   const double count = (double)(h - 1 - 2 * border) * (double)(w - 1 - 2 * border);
   moments_finalize_kernel<<<finalize_grid(n_sys), 320, 0, st>>>(a.partials, n_sys, p.units, count, sums);
   return check_launch("moments_finalize");
+}
+
+template <typename T>
+int launch(const T* frames, int64_t n_videos, int n_frames, int h, int w, int border, double* sums, void* ws,
+           size_t ws_size, void* dec, cudaStream_t st) {
+  if (n_frames - 1 <= 0 || n_videos == 0) return CT_OK;
+  if (pick_bc(w) == 128) return launch_bc<T, 128>(frames, n_videos, n_frames, h, w, border, sums, ws, ws_size, dec, st);
+  return launch_bc<T, 256>(frames, n_videos, n_frames, h, w, border, sums, ws, ws_size, dec, st);
 }
 
 }  // namespace

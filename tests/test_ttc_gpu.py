@@ -261,3 +261,19 @@ def test_blur_register_window_matches_smem_stage(monkeypatch, dtype, hw):
     monkeypatch.setenv("CT_BLUR_SMEM", "1")
     b = ct.run_sequence_batch(f[None], max_level=3).cpu().numpy()
     assert np.array_equal(np.nan_to_num(a, nan=7.0), np.nan_to_num(b, nan=7.0))
+
+
+@pytest.mark.parametrize("bc", ["128", "256"])
+def test_wide_frames_both_tile_widths_vs_oracle(monkeypatch, bc):
+    """Frames wider than one tile (several column tiles, TMA stride BC-4) with
+    either tile width agree with the oracle: fp64 TTC 1e-9, fp32 multiscale 1e-4."""
+    monkeypatch.setenv("CT_MOM_BC", bc)
+    f64 = O.generate(700, 90, 5, 60.0, (0.45, 0.5), 9, 0.0)
+    got = ct.run_sequence_batch(torch.from_numpy(f64).cuda()[None], level=0).cpu().numpy()[0]
+    ref = O.run_sequence(f64, level=0)
+    assert_est_close(got, ref, 1e-9)
+    f32 = f64.astype(np.float32)
+    got32 = ct.run_sequence_batch(torch.from_numpy(f32).cuda()[None], max_level=2).cpu().numpy()[0]
+    ref32 = O.run_sequence(f32.astype(np.float64), max_level=2)
+    assert np.array_equal(got32[:, 8], ref32[:, 8])
+    assert_est_close(got32, ref32, 1e-4, fields=(5,))
