@@ -277,3 +277,31 @@ def test_wide_frames_both_tile_widths_vs_oracle(monkeypatch, bc):
     ref32 = O.run_sequence(f32.astype(np.float64), max_level=2)
     assert np.array_equal(got32[:, 8], ref32[:, 8])
     assert_est_close(got32, ref32, 1e-4, fields=(5,))
+
+
+def test_randomized_shapes_levels_and_precisions():
+    """Seeded sweep over frame shapes around the tiling boundaries (band
+    heights, 255/256/257-column tiles, multi-tile strides), frame counts,
+    fixed levels and multiscale, both precisions, batched videos."""
+    rng = np.random.default_rng(2024)
+    shapes = [(17, 256), (33, 255), (48, 257), (65, 380), (16, 129), (100, 124), (31, 1000), (70, 508)]
+    for i, (h, w) in enumerate(shapes):
+        n = int(rng.integers(2, 6))
+        nv = int(rng.integers(1, 4))
+        vids = np.stack([O.generate(w, h, n, float(rng.uniform(30, 200)), (float(rng.uniform(0.3, 0.7)), 0.5),
+                                    100 + 10 * i + v, 0.002) for v in range(nv)])
+        dev = torch.from_numpy(vids).cuda()
+        lv = int(rng.integers(0, 2)) if min(h, w) >= 32 else 0
+        got = ct.run_sequence_batch(dev, level=lv).cpu().numpy()
+        for v in range(nv):
+            ref = O.run_sequence(vids[v], level=lv)
+            assert_est_close(got[v], ref, 1e-9)
+        if min(h, w) >= 64:
+            got = ct.run_sequence_batch(dev, max_level=2).cpu().numpy()
+            for v in range(nv):
+                assert_est_close(got[v], O.run_sequence(vids[v], max_level=2), 1e-9)
+        f32 = vids.astype(np.float32)
+        got = ct.run_sequence_batch(torch.from_numpy(f32).cuda(), level=0).cpu().numpy()
+        for v in range(nv):
+            ref = O.run_sequence(f32[v].astype(np.float64), level=0)
+            assert_est_close(got[v], ref, 1e-4, fields=(5,))
