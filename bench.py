@@ -168,11 +168,12 @@ def make_videos(V: int, seed0: int = 0):
     return frames
 
 
-def cpu_baseline_sample(seconds: float = 10.0):
-    """Oracle port on this host: cfg2 video repeated until ~`seconds` of CPU work."""
+def cpu_baseline_sample(seconds: float = 10.0, threads: int = 0):
+    """Oracle port on this host: cfg2 video repeated until ~`seconds` of CPU work
+    (threads = 0: every host thread; 1: the reference's serial setting)."""
     import oracle
     f = oracle.generate(W, H, NFRAMES, 100.0, (0.5, 0.5), 0, 0.0)
-    threads = len(os.sched_getaffinity(0))
+    threads = threads or len(os.sched_getaffinity(0))
     oracle.run_sequence(f[:4], level=0, nthreads=threads)  # warm
     n_est, t0 = 0, time.perf_counter()
     while time.perf_counter() - t0 < seconds:
@@ -425,6 +426,9 @@ def main():
         except Exception as exc:  # reported, never silently dropped
             secondary = {"error": repr(exc)}
     cpu = cpu_baseline_sample(args.cpu_seconds) if (rank == 0 and world == 1) else None
+    if cpu is not None:  # the reference is serial by design; report one core too
+        one = cpu_baseline_sample(min(3.0, args.cpu_seconds), threads=1)
+        cpu["one_core"] = {"value": one["value"], "unit": one["unit"], "cores": 1, "sample": one["sample"]}
 
     if rank == 0:
         line = {
