@@ -24,12 +24,14 @@
 // on scheduling (bit-reproducible run to run and across shard counts).
 #include <math.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include <algorithm>
 #include <type_traits>
 
 #include "common.cuh"
 #include "moments.cuh"
+#include "tma.cuh"
 
 namespace ct {
 namespace {
@@ -477,6 +479,121 @@ __global__ void __launch_bounds__(256) blur5_rows_kernel(const T* __restrict__ i
   }
 }
 
+// TMA-fed variant of blur5_rows_kernel: every warp streams its 32 x VX column
+// slab (plus 4 columns each side) through its own ring of RCH-row TMA boxes
+// (own mbarriers, no CTA-wide barriers), so many rows are in flight per SM
+// without registers; a lane reads its window (x-2 .. x+VX+1) from shared
+// memory.  REPLICATE clamping: rows outside the image reuse the nearest
+// image row's horizontal sums, columns outside take the edge value.  Same
+// FMA chains as blur5_rows_kernel (bit-identical).
+constexpr int kBlurRch = 4, kBlurStages = 4, kBlurWarps = 8;
+
+template <typename T>
+__global__ void __launch_bounds__(kBlurWarps * 32) blur5_tma_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                                     int64_t n_images, int dh, int dw, int strip,
+                                                                     T* __restrict__ out) {
+  constexpr int VX = 16 / sizeof(T);
+  constexpr int SC = 32 * VX + 2 * VX;  // staged columns per row: slab + VX each side (16-byte aligned)
+  constexpr int STAGE = kBlurRch * SC;  // elements per stage
+  using V = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+  extern __shared__ __align__(128) unsigned char smem_bl[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  T* ring = reinterpret_cast<T*>(smem_bl) + (size_t)wid * kBlurStages * STAGE;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_bl + (size_t)kBlurWarps * kBlurStages * STAGE * sizeof(T)) +
+                   wid * kBlurStages;
+  const T b5[5] = {T(1.0 / 16.0), T(4.0 / 16.0), T(6.0 / 16.0), T(4.0 / 16.0), T(1.0 / 16.0)};
+  if (lane == 0)
+    for (int k = 0; k < kBlurStages; ++k) mbar_init(&bars[k], 1);
+  __syncwarp();
+  if (lane == 0) mbar_fence_init();
+  __syncwarp();
+  const int warps_x = (dw + 32 * VX - 1) / (32 * VX);
+  const int n_strips = (dh + strip - 1) / strip;
+  const int64_t total = n_images * n_strips * warps_x;
+  const int64_t wstride = (int64_t)gridDim.x * kBlurWarps;
+  uint32_t uses = 0;  // boxes consumed by this warp (ring stage uses % S, phase (uses / S) & 1)
+  for (int64_t item = (int64_t)blockIdx.x * kBlurWarps + wid; item < total; item += wstride) {
+    const int wx = (int)(item % warps_x);
+    const int64_t t = item / warps_x;
+    const int si = (int)(t % n_strips);
+    const int64_t img = t / n_strips;
+    const int x0 = wx * 32 * VX;
+    const int x = x0 + lane * VX;
+    const bool valid = x < dw;
+    const int y0 = si * strip, y1 = min(dh, y0 + strip);
+    const int rs = max(0, y0 - 2), re = min(dh, y1 + 2);  // image rows this slab reads
+    const int nchunks = (re - rs + kBlurRch - 1) / kBlurRch;
+    const int64_t grow0 = img * (int64_t)dh + rs;  // tensor-map row of image row rs
+    auto issue = [&](int c) {
+      if (lane == 0) {
+        const uint32_t u = uses + c;
+        const int stg = u % kBlurStages;
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&bars[stg], (uint32_t)(STAGE * sizeof(T)));
+        tma_load_2d(ring + stg * STAGE, &tmap, &bars[stg], x0 - VX, (int)(grow0 + (int64_t)c * kBlurRch));
+      }
+    };
+    for (int c = 0; c < kBlurStages && c < nchunks; ++c) issue(c);
+    T h[5][VX];
+    T hcur[VX];
+    int have = -1;  // image row whose horizontal sums are in hcur
+    for (int yy = y0 - 2; yy < y1 + 2; ++yy) {
+      const int r = min(max(yy, 0), dh - 1);
+      if (r != have) {  // next image row of the stream (rows are visited in order)
+        const int ri = r - rs, c = ri / kBlurRch;
+        const uint32_t u = uses + c;
+        const int stg = u % kBlurStages;
+        if (ri % kBlurRch == 0) mbar_wait(&bars[stg], (u / kBlurStages) & 1);
+        const T* row = ring + stg * STAGE + (ri % kBlurRch) * SC + lane * VX;  // staged col 0 = x0 - VX
+        T m[3 * VX];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          const V v = *reinterpret_cast<const V*>(row + q * VX);
+          const T* vv = reinterpret_cast<const T*>(&v);
+#pragma unroll
+          for (int e = 0; e < VX; ++e) m[q * VX + e] = vv[e];
+        }
+        // window x-2 .. x+VX+1 = m[VX-2 .. 2VX+1]
+        if (x == 0) m[VX - 2] = m[VX - 1] = m[VX];
+        if (valid && x + VX >= dw) m[2 * VX] = m[2 * VX + 1] = m[2 * VX - 1];
+        else if (valid && x + VX + 1 >= dw) m[2 * VX + 1] = m[2 * VX];
+#pragma unroll
+        for (int cc = 0; cc < VX; ++cc) {
+          T acc = T(0);
+#pragma unroll
+          for (int j1 = 0; j1 < 5; ++j1) acc = fmx(b5[j1], m[VX - 2 + cc + j1], acc);
+          hcur[cc] = acc;
+        }
+        have = r;
+        if (ri % kBlurRch == kBlurRch - 1 || r == re - 1) {  // chunk fully read: refill its stage
+          __syncwarp();
+          if (c + kBlurStages < nchunks) issue(c + kBlurStages);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int cc = 0; cc < VX; ++cc) h[k][cc] = h[k + 1][cc];
+#pragma unroll
+      for (int cc = 0; cc < VX; ++cc) h[4][cc] = hcur[cc];
+      if (yy >= y0 + 2 && valid) {
+        V o;
+        T* ov = reinterpret_cast<T*>(&o);
+#pragma unroll
+        for (int cc = 0; cc < VX; ++cc) {
+          T acc = T(0);
+#pragma unroll
+          for (int j0 = 0; j0 < 5; ++j0) acc = fmx(b5[j0], h[j0][cc], acc);
+          ov[cc] = acc;
+        }
+        *reinterpret_cast<V*>(out + (img * (int64_t)dh + (yy - 2)) * dw + x) = o;
+      }
+    }
+    uses += nchunks;
+    __syncwarp();
+  }
+}
+
 // Second half of downsample: 5x5 binomial SAME/REPLICATE over already
 // decimated images (dh x dw each, from the fused moments kernel).
 template <typename T>
@@ -484,8 +601,28 @@ int launch_blur_dec(const T* dec, int64_t n_images, int h, int w, T* out, cudaSt
   const int dh = h / 2, dw = w / 2;
   if (n_images == 0 || dh == 0 || dw == 0) return CT_OK;
   constexpr int VX = 16 / sizeof(T);
-  if (dw % VX == 0 && reinterpret_cast<uintptr_t>(dec) % 16 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0 &&
-      !getenv("CT_BLUR_SMEM")) {
+  const bool aligned = dw % VX == 0 && reinterpret_cast<uintptr_t>(dec) % 16 == 0 &&
+                       reinterpret_cast<uintptr_t>(out) % 16 == 0;
+  if (aligned && !getenv("CT_BLUR_SMEM") && !getenv("CT_BLUR_REGS") && n_images * dh < (1ll << 31)) {
+    CUtensorMap tmap;
+    memset(&tmap, 0, sizeof(tmap));
+    constexpr int SC = 32 * VX + 2 * VX;
+    if (encode_tmap_2d(&tmap, dec, sizeof(T), (uint64_t)dw, (uint64_t)(n_images * dh), SC, kBlurRch)) {
+      int strip = 64;
+      while (strip > 8 && n_images * cdiv(dh, strip) * cdiv(dw, 32 * VX) < (int64_t)num_sms() * 24) strip /= 2;
+      const int64_t items = n_images * cdiv(dh, strip) * cdiv(dw, 32 * VX);
+      const size_t smem = (size_t)kBlurWarps * kBlurStages * kBlurRch * SC * sizeof(T) +
+                          kBlurWarps * kBlurStages * sizeof(uint64_t);
+      auto kern = blur5_tma_kernel<T>;
+      CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      int per_sm = 1;
+      CT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlurWarps * 32, smem));
+      const int64_t blocks = std::min<int64_t>(cdiv(items, kBlurWarps), (int64_t)num_sms() * std::max(1, per_sm));
+      kern<<<(unsigned)blocks, kBlurWarps * 32, smem, st>>>(tmap, n_images, dh, dw, strip, out);
+      return check_launch("pyramid_blur_tma");
+    }
+  }
+  if (aligned && !getenv("CT_BLUR_SMEM")) {
     // row strips per warp: as long as possible (the 4 halo rows are re-read)
     // while keeping >= 16 warps per SM busy
     int strip = 64;

@@ -251,16 +251,21 @@ def test_batched_textures_match_single():
 
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
-@pytest.mark.parametrize("hw", [(270, 480), (135, 244), (66, 130), (101, 77)])
-def test_blur_register_window_matches_smem_stage(monkeypatch, dtype, hw):
-    """The register sliding-window blur (blur5_rows_kernel) and the shared-memory
-    stage it replaces use the same FMA chains: multiscale estimates must be
-    bit-identical (odd widths take the shared-memory stage either way)."""
+@pytest.mark.parametrize("hw", [(270, 480), (135, 244), (66, 130), (101, 77), (9, 1100), (300, 36)])
+def test_blur_variants_bit_identical(monkeypatch, dtype, hw):
+    """The three multiscale blur stages (TMA-fed per-warp window, register
+    window with global loads, shared-memory tile) use the same FMA chains:
+    multiscale estimates must be bit-identical (odd widths take the
+    shared-memory stage in every mode)."""
     f = torch.from_numpy(O.generate(hw[1], hw[0], 5, 80.0, (0.4, 0.55), 3, 0.0)).to(dtype).cuda()
-    a = ct.run_sequence_batch(f[None], max_level=3).cpu().numpy()
+    lv = 3 if min(hw) >= 64 else 1
+    a = ct.run_sequence_batch(f[None], max_level=lv).cpu().numpy()
+    monkeypatch.setenv("CT_BLUR_REGS", "1")
+    b = ct.run_sequence_batch(f[None], max_level=lv).cpu().numpy()
     monkeypatch.setenv("CT_BLUR_SMEM", "1")
-    b = ct.run_sequence_batch(f[None], max_level=3).cpu().numpy()
+    c = ct.run_sequence_batch(f[None], max_level=lv).cpu().numpy()
     assert np.array_equal(np.nan_to_num(a, nan=7.0), np.nan_to_num(b, nan=7.0))
+    assert np.array_equal(np.nan_to_num(a, nan=7.0), np.nan_to_num(c, nan=7.0))
 
 
 @pytest.mark.parametrize("bc", ["128", "256"])
