@@ -281,6 +281,11 @@ __global__ void __launch_bounds__(256) xcorr_generic(const GenArgs a) {
 template <typename T>
 constexpr int tma_vx() { return 16 / sizeof(T); }
 
+#ifndef CT_TMA2D_STAGES
+#define CT_TMA2D_STAGES 2
+#endif
+constexpr int kTma2dStages = CT_TMA2D_STAGES;  // TMA ring depth of the 2-D conv kernel
+
 template <typename T, int NW, int VX, int TY, int NH>
 __global__ void __launch_bounds__(256) xcorr_tma2d(const TileArgs a, const __grid_constant__ TapsParam<T> taps,
                                                    const __grid_constant__ CUtensorMap tmap) {
@@ -295,7 +300,7 @@ __global__ void __launch_bounds__(256) xcorr_tma2d(const TileArgs a, const __gri
   const int64_t n_tiles = (int64_t)tiles_x * tiles_y * a.batch;
   const size_t stage_bytes = ((size_t)a.sx * a.sy * sizeof(T) + 127) & ~size_t(127);
   auto stage = [&](int s) { return reinterpret_cast<T*>(smem_tma + (size_t)s * stage_bytes); };
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_tma + 2 * stage_bytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_tma + kTma2dStages * stage_bytes);
   const uint32_t box_bytes = (uint32_t)(a.sx * a.sy * sizeof(T));
   const int ny = a.ny;
 
@@ -312,19 +317,17 @@ __global__ void __launch_bounds__(256) xcorr_tma2d(const TileArgs a, const __gri
     tma_load_3d(stage(s), &tmap, &bars[s], x0 - a.px, y0 - a.py, b);
   };
   if (tid == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+    for (int k = 0; k < kTma2dStages; ++k) mbar_init(&bars[k], 1);
     mbar_fence_init();
   }
   __syncthreads();
   int64_t t = blockIdx.x;
-  if (tid == 0) {
-    if (t < n_tiles) issue(t, 0);
-    if (t + gridDim.x < n_tiles) issue(t + gridDim.x, 1);
-  }
+  if (tid == 0)
+    for (int k = 0; k < kTma2dStages; ++k)
+      if (t + k * (int64_t)gridDim.x < n_tiles) issue(t + k * (int64_t)gridDim.x, k);
   for (int it = 0; t < n_tiles; ++it, t += gridDim.x) {
-    const int s = it & 1;
-    mbar_wait(&bars[s], (uint32_t)((it >> 1) & 1));
+    const int s = it % kTma2dStages;
+    mbar_wait(&bars[s], (uint32_t)((it / kTma2dStages) & 1));
     const T* tile = stage(s);
     T acc[TY][VX];
 #pragma unroll
@@ -360,10 +363,10 @@ __global__ void __launch_bounds__(256) xcorr_tma2d(const TileArgs a, const __gri
         }
       }
     }
-    __syncthreads();  // stage s fully read: refill it with the tile two steps ahead
-    if (tid == 0 && t + 2 * (int64_t)gridDim.x < n_tiles) {
+    __syncthreads();  // stage s fully read: refill it with the tile kTma2dStages steps ahead
+    if (tid == 0 && t + kTma2dStages * (int64_t)gridDim.x < n_tiles) {
       fence_proxy_async_smem();
-      issue(t + 2 * (int64_t)gridDim.x, s);
+      issue(t + kTma2dStages * (int64_t)gridDim.x, s);
     }
     int x0, y0, b;
     tile_coords(t, x0, y0, b);
@@ -409,7 +412,7 @@ int launch_tma2d(const TileArgs& a0, const T* taps_host, int ntaps, cudaStream_t
     return CT_EUNSUPPORTED;
   }
   const size_t stage_bytes = ((size_t)a.sx * a.sy * sizeof(T) + 127) & ~size_t(127);
-  const size_t smem = 2 * stage_bytes + 16;
+  const size_t smem = kTma2dStages * stage_bytes + 8 * kTma2dStages;
   auto kern = xcorr_tma2d<T, NW, VX, TY, NH>;
   CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
