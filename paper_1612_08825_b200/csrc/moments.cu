@@ -419,23 +419,31 @@ __global__ void __launch_bounds__(BC, 512 / BC) ttc_moments_kernel(const MomentA
 }
 
 // sums[sys] = fixed-order sum of the `units` band partials of each system.
-// One warp per (system, value): lanes take units lane, lane+32, ... and a
-// butterfly combines them (fixed tree -> deterministic).
-__global__ void __launch_bounds__(320) moments_finalize_kernel(const double* partials, int64_t n_sys, int units,
-                                                               double count, double* sums) {
-  const int q = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int64_t sys = blockIdx.x; sys < n_sys; sys += gridDim.x) {
-    const double* p = partials + sys * units * 10 + q;
-    double acc = 0.0;
-    for (int u = lane; u < units; u += 32) acc += p[(int64_t)u * 10];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) sums[sys * 11 + q] = acc;
-    if (threadIdx.x == 0) sums[sys * 11 + 10] = count;
+// One warp per system: lane q < 10 adds value q of units 0, 1, 2, ... in
+// order (each step of the warp reads one 80-byte partial row, coalesced);
+// the fixed order keeps results bit-reproducible.  Persistent: a few
+// resident blocks per SM walk the systems.
+constexpr int kFinWarps = 8;
+__global__ void __launch_bounds__(kFinWarps * 32) moments_finalize_kernel(const double* partials, int64_t n_sys,
+                                                                         int units, double count, double* sums) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * kFinWarps;
+  for (int64_t sys = (int64_t)blockIdx.x * kFinWarps + (threadIdx.x >> 5); sys < n_sys; sys += nwarps) {
+    if (lane < 10) {
+      const double* p = partials + sys * units * 10 + lane;
+      double acc = 0.0;
+#pragma unroll 8
+      for (int u = 0; u < units; ++u) acc += p[(int64_t)u * 10];
+      sums[sys * 11 + lane] = acc;
+    } else if (lane == 10) {
+      sums[sys * 11 + 10] = count;
+    }
   }
 }
 
-inline unsigned finalize_grid(int64_t n_sys) { return (unsigned)std::min<int64_t>(n_sys, 65535); }
+inline unsigned finalize_grid(int64_t n_sys) {
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n_sys, kFinWarps), (int64_t)num_sms() * 8));
+}
 
 // Band height: 16 rows for f64 (3 x 35 KB buffers, 2 CTAs/SM, FP64-bound),
 // 32 rows for f32 (3 x 34 KB; the cheaper FP32 math needs bigger TMA
@@ -554,7 +562,7 @@ int launch_bc(const T* frames, int64_t n_videos, int n_frames, int h, int w, int
   if (rc) return rc;
   const int64_t n_sys = n_videos * n_pairs;
   const double count = (double)(h - 1 - 2 * border) * (double)(w - 1 - 2 * border);
-  moments_finalize_kernel<<<finalize_grid(n_sys), 320, 0, st>>>(a.partials, n_sys, p.units, count, sums);
+  moments_finalize_kernel<<<finalize_grid(n_sys), kFinWarps * 32, 0, st>>>(a.partials, n_sys, p.units, count, sums);
   return check_launch("moments_finalize");
 }
 
@@ -582,7 +590,7 @@ int moments_launch(int dtype, const void* frames, int64_t n_videos, int n_frames
 int partials_finalize(const double* partials, int64_t n_sys, int units, double count, double* sums,
                       cudaStream_t st) {
   if (n_sys == 0) return CT_OK;
-  moments_finalize_kernel<<<finalize_grid(n_sys), 320, 0, st>>>(partials, n_sys, units, count, sums);
+  moments_finalize_kernel<<<finalize_grid(n_sys), kFinWarps * 32, 0, st>>>(partials, n_sys, units, count, sums);
   return check_launch("moments_finalize");
 }
 
