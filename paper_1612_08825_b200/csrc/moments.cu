@@ -45,6 +45,10 @@ namespace {
 // start 16-byte aligned (a start at element 255 faults with an illegal
 // instruction), and 252 is a multiple of 4 f32 / 2 f64 elements.
 // (multi-tile stride: BC - 4 grid columns)
+#ifndef CT_MOM_TWO_COL_F32
+#define CT_MOM_TWO_COL_F32 1
+#endif
+constexpr bool kTwoColF32 = CT_MOM_TWO_COL_F32;  // fp32: two grid columns per thread (sweep_c2)
 #ifndef CT_MOM_PACKED_F32
 #define CT_MOM_PACKED_F32 1
 #endif
@@ -99,15 +103,15 @@ __device__ __forceinline__ void write_dec(const MomentArgs& a, const T* buf, int
   }
 }
 
-template <typename T, int BR, int NB, int BC>
-struct Smem {  // NB = frame-band buffers in the TMA ring (NB - 2 frames in flight per pair)
+template <typename T, int BR, int NB, int BC, int NT = BC>
+struct Smem {  // NB = frame-band buffers in the TMA ring (NB - 2 frames in flight per pair), NT threads
   static constexpr size_t buf_elems = (size_t)(BR + 1) * BC + 8;  // +8: masked right-neighbour reads
   static constexpr size_t buf_bytes = (buf_elems * sizeof(T) + 127) & ~size_t(127);
   // the reduction scratch lives in the dead previous-frame buffer; f32 bands
   // are smaller, so lane pairs are combined first (half the scratch)
-  static constexpr bool half_red = buf_bytes < 10 * BC * sizeof(double);
-  static constexpr int red_n = half_red ? BC / 2 : BC;
-  static constexpr int seg = BC >= 256 ? 16 : 8;  // stage-1 segments per value (10 * seg <= BC threads)
+  static constexpr bool half_red = buf_bytes < 10 * NT * sizeof(double);
+  static constexpr int red_n = half_red ? NT / 2 : NT;
+  static constexpr int seg = NT >= 256 ? 16 : NT >= 128 ? 8 : 4;  // stage-1 segments per value (10 * seg <= NT)
   static_assert(buf_bytes >= 10 * (size_t)red_n * sizeof(double), "reduction scratch must fit a band buffer");
   static constexpr size_t bars_off = NB * buf_bytes;
   static constexpr size_t part_off = bars_off + 64;
@@ -267,12 +271,84 @@ __device__ __forceinline__ void sweep_x2(const float* __restrict__ A, const floa
   m[9] = u4x + fmaf(K * K, s3.y, fmaf(2 * K, u2y, u4y));
 }
 
-template <typename T, int BR, int NB, int BC>
-__global__ void __launch_bounds__(BC, 512 / BC) ttc_moments_kernel(const MomentArgs a,
-                                                                  const __grid_constant__ CUtensorMap tmap) {
+// fp32 two-column sweep: a thread owns grid columns col, col+1 and keeps
+// them as the two lanes of packed f32x2 registers.  Per frame row it reads
+// (F[col], F[col+1]) as one 8-byte load plus F[col+2] (half the shared-memory
+// loads of one column per thread); the shifted pairs (P1, P2), (D1, D2) are
+// assembled with moves.  m[c] are column c's ten sums (same per-lane
+// operation order as sweep()).
+template <int BR, bool CHECK, int BC>
+__device__ __forceinline__ void sweep_c2(const float* __restrict__ A, const float* __restrict__ B, int col, int r_beg,
+                                         int r_end, float (&m)[2][10]) {
+  float2 s1 = {0, 0}, s2 = {0, 0}, s3 = {0, 0}, s4 = {0, 0}, s5 = {0, 0}, s6 = {0, 0};
+  float2 q2 = {0, 0}, q3 = {0, 0}, q5 = {0, 0}, qq3 = {0, 0};
+  float2 hP, dP, sD;
+  auto row = [&](int r, float2& P01, float2& P12, float2& D01, float2& D12) {
+    const float2 a01 = *reinterpret_cast<const float2*>(A + r * BC + col);
+    const float2 b01 = *reinterpret_cast<const float2*>(B + r * BC + col);
+    const float a2 = A[r * BC + col + 2], b2 = B[r * BC + col + 2];
+    P01 = f2add(a01, b01);
+    D01 = f2sub(b01, a01);
+    P12 = make_float2(P01.y, a2 + b2);
+    D12 = make_float2(D01.y, b2 - a2);
+  };
+  {
+    float2 P01, P12, D01, D12;
+    row(0, P01, P12, D01, D12);
+    hP = f2add(P01, P12);
+    dP = f2sub(P12, P01);
+    sD = f2add(D01, D12);
+  }
+#pragma unroll
+  for (int r = 1; r <= BR; ++r) {
+    float2 P01, P12, D01, D12;
+    row(r, P01, P12, D01, D12);
+    const float2 nhP = f2add(P01, P12), ndP = f2sub(P12, P01), nsD = f2add(D01, D12);
+    if (!CHECK || (r >= r_beg && r <= r_end)) {
+      const float2 ex = f2add(dP, ndP), ey = f2sub(nhP, hP), et = f2add(sD, nsD);
+      s1 = f2fma(ex, ex, s1);
+      s2 = f2fma(ex, ey, s2);
+      s3 = f2fma(ey, ey, s3);
+      s4 = f2fma(ex, et, s4);
+      s5 = f2fma(ey, et, s5);
+      s6 = f2fma(et, et, s6);
+    }
+    if (r == 1) {
+      q2 = s2;
+      q3 = s3;
+      q5 = s5;
+      qq3 = s3;
+    } else {
+      q2 = f2add(q2, s2);
+      q3 = f2add(q3, s3);
+      q5 = f2add(q5, s5);
+      qq3 = f2add(qq3, q3);
+    }
+    hP = nhP;
+    dP = ndP;
+    sD = nsD;
+  }
+  constexpr float K = float(BR);
+  const float2 S[6] = {s1, s2, s3, s4, s5, s6};
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    auto L = [&](float2 v) { return c ? v.y : v.x; };
+#pragma unroll
+    for (int k = 0; k < 6; ++k) m[c][k] = L(S[k]);
+    m[c][6] = fmaf(K, L(s2), -L(q2));
+    m[c][7] = fmaf(K, L(s3), -L(q3));
+    m[c][8] = fmaf(K, L(s5), -L(q5));
+    m[c][9] = fmaf(K * K, L(s3), fmaf(-(2 * K + 1), L(q3), 2 * L(qq3)));
+  }
+}
+
+template <typename T, int BR, int NB, int BC, int CPT>
+__global__ void __launch_bounds__(BC / CPT, 512 / BC) ttc_moments_kernel(const MomentArgs a,
+                                                                        const __grid_constant__ CUtensorMap tmap) {
   using ACC = typename AccT<T>::type;
-  using S = Smem<T, BR, NB, BC>;
-  constexpr int kThreads = BC;
+  constexpr int kThreads = BC / CPT;
+  using S = Smem<T, BR, NB, BC, kThreads>;
+  static_assert(CPT == 1 || sizeof(T) == 4, "two columns per thread is the fp32 path");
   constexpr int kRedSeg = S::seg;
   extern __shared__ __align__(128) unsigned char smem[];
   auto buf = [&](int k) { return reinterpret_cast<T*>(smem + (size_t)k * S::buf_bytes); };
@@ -292,9 +368,15 @@ __global__ void __launch_bounds__(BC, 512 / BC) ttc_moments_kernel(const MomentA
   const int nload = p1 - p0 + 1;
   constexpr uint32_t kBoxBytes = (uint32_t)((BR + 1) * BC * sizeof(T));
 
-  const int gx = cx0 + tid;
-  const bool in_col = tid < a.tile_cols && gx >= a.border && gx < a.gw - a.border;
-  const double xc = (double)gx - (double)(a.gw - 1) / 2.0;
+  const int col = tid * CPT;  // first tile column of this thread
+  bool in_col[CPT];
+  double xc[CPT];
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) {
+    const int gx = cx0 + col + c;
+    in_col[c] = col + c < a.tile_cols && gx >= a.border && gx < a.gw - a.border;
+    xc[c] = (double)gx - (double)(a.gw - 1) / 2.0;
+  }
   const double yc0 = (double)gy0 - (double)(a.gh - 1) / 2.0;    // centred y of grid row gy0
   const int64_t row0 = (v * a.n_frames) * (int64_t)a.h + gy0;  // band row of frame p: row0 + p*h
   // band-local frame-row range r in [r_beg, r_end] whose grid row gy0 + r - 1 is interior
@@ -348,37 +430,44 @@ __global__ void __launch_bounds__(BC, 512 / BC) ttc_moments_kernel(const MomentA
       write_dec<T, BR, kThreads, BC>(a, A, v, p, gy0, cx0, tid);
       if (p1 == n_pairs && i == p1 - p0 - 1) write_dec<T, BR, kThreads, BC>(a, B, v, p1, gy0, cx0, tid);
     }
-    ACC m[10];
-    if (r_beg <= 1 && r_end >= BR) {
-      if constexpr (sizeof(T) == 4 && kPackedF32)
-        sweep_x2<BR, BC>(A, B, tid, m);
+    ACC mc[CPT][10];
+    if constexpr (CPT == 2) {
+      if (r_beg <= 1 && r_end >= BR)
+        sweep_c2<BR, false, BC>(reinterpret_cast<const float*>(A), reinterpret_cast<const float*>(B), col, 1, BR, mc);
       else
-        sweep<T, BR, false, BC>(A, B, tid, 1, BR, m);
+        sweep_c2<BR, true, BC>(reinterpret_cast<const float*>(A), reinterpret_cast<const float*>(B), col, r_beg, r_end,
+                               mc);
     } else {
-      sweep<T, BR, true, BC>(A, B, tid, r_beg, r_end, m);
+      ACC(&m)[10] = mc[0];
+      if (r_beg <= 1 && r_end >= BR) {
+        if constexpr (sizeof(T) == 4 && kPackedF32)
+          sweep_x2<BR, BC>(A, B, col, m);
+        else
+          sweep<T, BR, false, BC>(A, B, col, 1, BR, m);
+      } else {
+        sweep<T, BR, true, BC>(A, B, col, r_beg, r_end, m);
+      }
     }
 
     // this thread's ten sums, order m00 m01 m02 m11 m12 m22 r0 r1 r2 et2 (rhs not yet negated)
     double o[10];
-    if (in_col) {
-      const double S1 = m[0], S2 = m[1], S3 = m[2], S4 = m[3], S5 = m[4], S6 = m[5];
-      const double U1 = fma(yc0, S2, (double)m[6]);
-      const double U2 = fma(yc0, S3, (double)m[7]);
-      const double U3 = fma(yc0, S5, (double)m[8]);
-      const double U4 = fma(yc0 * yc0, S3, fma(2.0 * yc0, (double)m[7], (double)m[9]));
-      o[0] = S1;
-      o[1] = S2;
-      o[2] = fma(xc, S1, U1);
-      o[3] = S3;
-      o[4] = fma(xc, S2, U2);
-      o[5] = fma(xc * xc, S1, fma(2.0 * xc, U1, U4));
-      o[6] = S4;
-      o[7] = S5;
-      o[8] = fma(xc, S4, U3);
-      o[9] = S6;
-    } else {
 #pragma unroll
-      for (int q = 0; q < 10; ++q) o[q] = 0.0;
+    for (int q = 0; q < 10; ++q) o[q] = 0.0;
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      if (in_col[c]) {
+        const ACC(&m)[10] = mc[c];
+        const double S1 = m[0], S2 = m[1], S3 = m[2], S4 = m[3], S5 = m[4], S6 = m[5];
+        const double U1 = fma(yc0, S2, (double)m[6]);
+        const double U2 = fma(yc0, S3, (double)m[7]);
+        const double U3 = fma(yc0, S5, (double)m[8]);
+        const double U4 = fma(yc0 * yc0, S3, fma(2.0 * yc0, (double)m[7], (double)m[9]));
+        const double X = xc[c];
+        const double v[10] = {S1, S2, fma(X, S1, U1), S3, fma(X, S2, U2), fma(X * X, S1, fma(2.0 * X, U1, U4)),
+                              S4, S5, fma(X, S4, U3), S6};
+#pragma unroll
+        for (int q = 0; q < 10; ++q) o[q] = CPT == 1 ? v[q] : o[q] + v[q];
+      }
     }
     double* red = reinterpret_cast<double*>(const_cast<T*>(A));  // frame p0+i is dead after the sweep
     if (S::half_red) {
@@ -419,9 +508,10 @@ __global__ void __launch_bounds__(BC, 512 / BC) ttc_moments_kernel(const MomentA
 }
 
 // sums[sys] = fixed-order sum of the `units` band partials of each system.
-// One warp per system: lane q < 10 adds value q of units 0, 1, 2, ... in
-// order (each step of the warp reads one 80-byte partial row, coalesced);
-// the fixed order keeps results bit-reproducible.  Persistent: a few
+// One warp per system: lane l adds the partial rows u = l, l+32, ... (each
+// row is 10 contiguous doubles, so a warp step reads 32 consecutive rows,
+// coalesced), then a fixed butterfly combines the lanes; the order depends
+// only on `units`, so results are bit-reproducible.  Persistent: a few
 // resident blocks per SM walk the systems.
 constexpr int kFinWarps = 8;
 __global__ void __launch_bounds__(kFinWarps * 32) moments_finalize_kernel(const double* partials, int64_t n_sys,
@@ -429,13 +519,25 @@ __global__ void __launch_bounds__(kFinWarps * 32) moments_finalize_kernel(const 
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * kFinWarps;
   for (int64_t sys = (int64_t)blockIdx.x * kFinWarps + (threadIdx.x >> 5); sys < n_sys; sys += nwarps) {
-    if (lane < 10) {
-      const double* p = partials + sys * units * 10 + lane;
-      double acc = 0.0;
-#pragma unroll 8
-      for (int u = 0; u < units; ++u) acc += p[(int64_t)u * 10];
-      sums[sys * 11 + lane] = acc;
-    } else if (lane == 10) {
+    double acc[10];
+#pragma unroll
+    for (int q = 0; q < 10; ++q) acc[q] = 0.0;
+    for (int u = lane; u < units; u += 32) {
+      const double2* r = reinterpret_cast<const double2*>(partials + (sys * units + u) * 10);
+#pragma unroll
+      for (int k = 0; k < 5; ++k) {
+        const double2 v = r[k];
+        acc[2 * k] += v.x;
+        acc[2 * k + 1] += v.y;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 10; ++q)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+    if (lane == 0) {
+#pragma unroll
+      for (int q = 0; q < 10; ++q) sums[sys * 11 + q] = acc[q];
       sums[sys * 11 + 10] = count;
     }
   }
@@ -471,20 +573,14 @@ struct Plan {
   int n_bands, n_ctiles, units, chunk, n_chunks, tile_cols;
 };
 
-// Tile width: 256 columns, or 128 (4 CTAs of 4 warps per SM instead of 2 of
-// 8, so the per-pair barriers of different CTAs overlap better) when the
-// frame needs several tiles anyway and 128-wide tiles load no more columns.
-// Measured on cfg5 (1080x1920 f32): 128 is 4.5% faster; on 256-wide frames
-// 256 (one tile) is much faster.
-inline int tile_loaded_cols(int gw, int bc) {
-  const int tc = gw <= bc - 1 ? bc - 1 : bc - 4;
-  return (gw + tc - 1) / tc * bc;
-}
+// Tile width: 256 columns.  128-column tiles (4 CTAs of 4 warps per SM) were
+// 4.5 % faster on 1080x1920 fp32 with one column per thread, but with two
+// columns per thread (fp32) and for fp64 the 256-column tiles win on wide
+// frames too (profiles/r01_moments_probe.md); 128 stays selectable for probing.
 inline int pick_bc(int w) {
-  if (const char* e = getenv("CT_MOM_BC")) return atoi(e) == 128 ? 128 : 256;  // probing only
-  const int gw = w - 1;
-  if (gw <= 255) return 256;
-  return tile_loaded_cols(gw, 128) <= tile_loaded_cols(gw, 256) ? 128 : 256;
+  (void)w;
+  if (const char* e = getenv("CT_MOM_BC")) return atoi(e) == 128 ? 128 : 256;  // probing / tests only
+  return 256;
 }
 
 template <typename T, int BC>
@@ -553,11 +649,12 @@ int launch_bc(const T* frames, int64_t n_videos, int n_frames, int h, int w, int
   a.use_tma = !no_tma && encode_tmap_2d(&tmap, frames, sizeof(T), (uint64_t)w,
                                         (uint64_t)(n_videos * n_frames * (int64_t)h), BC, BR + 1);
   constexpr int NB = ring_buffers<T>();
-  using S = Smem<T, BR, NB, BC>;
-  auto kern = ttc_moments_kernel<T, BR, NB, BC>;
+  constexpr int CPT = (sizeof(T) == 4 && kTwoColF32 && BC == 256) ? 2 : 1;
+  using S = Smem<T, BR, NB, BC, BC / CPT>;
+  auto kern = ttc_moments_kernel<T, BR, NB, BC, CPT>;
   CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::total));
   dim3 grid((unsigned)p.units, (unsigned)p.n_chunks, (unsigned)n_videos);
-  kern<<<grid, BC, S::total, st>>>(a, tmap);
+  kern<<<grid, BC / CPT, S::total, st>>>(a, tmap);
   int rc = check_launch("ttc_moments");
   if (rc) return rc;
   const int64_t n_sys = n_videos * n_pairs;
