@@ -112,6 +112,19 @@ int ct_pyramid_down(int dtype, const void* in, int64_t n_images, int64_t h, int6
 int ct_ttc_multiscale_select(const double* est_levels, int64_t count, int n_levels, double* best,
                              void* stream);
 
+/* Multiscale normal-system sums (SURVEY.md 8(b) ct_ttc_pyramid_moments): for
+ * pyramid levels l = 0..levels-1 (level l = l-fold ttc.downsample of the
+ * frames, ttc.py:187-204) the 11 sums of every consecutive pair, as
+ * ttc_moments writes them, laid out [levels][n_videos][n_frames-1][11].  These
+ * are the systems estimate_multiscale solves per level (ttc.py:248-279).
+ * Errors: fewer than two frames, levels outside [1, 30], or a level smaller
+ * than 4 pixels (the reference's _level_extents guard, ttc.py:235-241). */
+size_t ct_ttc_pyramid_moments_workspace_bytes(int dtype, int64_t n_videos, int64_t n_frames, int64_t h,
+                                              int64_t w, int levels);
+int ct_ttc_pyramid_moments(int dtype, const void* frames, int64_t n_videos, int64_t n_frames, int64_t h,
+                           int64_t w, int levels, double* sums, void* workspace, size_t workspace_bytes,
+                           void* stream);
+
 /* run_sequence for `n_videos` independent stacks [n_videos][n_frames][h][w]:
  * max_level < 0 -> estimate_fixed(level), else estimate_multiscale(max_level).
  * Writes est[n_videos][n_frames-1][10]; a `None` multiscale result has level -1. */

@@ -36,6 +36,7 @@ from .ttc import (
     radial_gradient,
     run_sequence,
     run_sequence_batch,
+    pyramid_moments,
     run_sequence_host,
     solve_ttc,
     trace_lines,

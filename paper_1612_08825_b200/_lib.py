@@ -31,6 +31,7 @@ EXPORTS = (
     "ct_ttc_multiscale_select", "ct_run_sequence_workspace_bytes", "ct_run_sequence",
     "ct_run_sequence_host_workspace_bytes", "ct_run_sequence_host", "ct_zoom_frames",
     "ct_zoom_frames_workspace_bytes", "ct_gradient", "ct_decode_samples",
+    "ct_ttc_pyramid_moments_workspace_bytes", "ct_ttc_pyramid_moments",
 )
 
 _lib = None
@@ -72,6 +73,9 @@ def load(require_gpu: bool = True):
         L.ct_zoom_frames_workspace_bytes.restype = SZ
         L.ct_gradient.argtypes = [I, P, I64, I64, I64, P, P, I64, I64, P, P, P, P, P]
         L.ct_decode_samples.argtypes = [I, P, I64, D, P, P]
+        L.ct_ttc_pyramid_moments_workspace_bytes.argtypes = [I, I64, I64, I64, I64, I]
+        L.ct_ttc_pyramid_moments_workspace_bytes.restype = SZ
+        L.ct_ttc_pyramid_moments.argtypes = [I, P, I64, I64, I64, I64, I, P, P, SZ, P]
         _lib = L
     if require_gpu and not torch.cuda.is_available():
         raise RuntimeError("convtact_b200 needs a CUDA device (sm_100a); there is no CPU fallback")

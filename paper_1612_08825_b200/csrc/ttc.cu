@@ -749,6 +749,69 @@ int run_seq(const T* frames, int64_t nv, int nf, int h, int w, int level, int ma
   return check_launch("multiscale_select");
 }
 
+// Per-level normal-system sums of every frame pair on the multiscale pyramid
+// (the `[n-1][levels][11]` entry SURVEY.md 8(b) proposes, here laid out
+// [levels][n_videos][n_frames-1][11]): level l is the l-fold downsample of the
+// frames (block means fused into the previous level's moments kernel, then
+// the 5x5 binomial), exactly the sums run_sequence's multiscale walk solves.
+template <typename T>
+size_t pyr_ws(int64_t nv, int nf, int h, int w, int levels) {
+  const int dt = sizeof(T) == 8 ? CT_F64 : CT_F32;
+  size_t total = 0, mom = 0;
+  int lh = h, lw = w;
+  for (int l = 0; l < levels; ++l) {
+    if (l > 0) total += align256((size_t)nv * nf * lh * lw * sizeof(T));
+    mom = std::max(mom, moments_workspace(dt, nv, nf, lh, lw));
+    lh /= 2;
+    lw /= 2;
+  }
+  if (levels > 1) total += align256((size_t)nv * nf * (h / 2) * (w / 2) * sizeof(T));
+  return total + align256(mom);
+}
+
+template <typename T>
+int pyr_moments(const T* frames, int64_t nv, int nf, int h, int w, int levels, double* sums, void* ws,
+                size_t ws_bytes, cudaStream_t st) {
+  const int64_t np = nv * (nf - 1);
+  if (np <= 0) return CT_OK;
+  const size_t need = pyr_ws<T>(nv, nf, h, w, levels);
+  CT_REQUIRE(ws != nullptr && ws_bytes >= need, "pyramid_moments workspace too small (%zu < %zu)", ws_bytes, need);
+  const int dt = sizeof(T) == 8 ? CT_F64 : CT_F32;
+  char* cur = reinterpret_cast<char*>(ws);
+  const T* level_ptr[32];
+  T* level_buf[32] = {nullptr};
+  int level_h[32], level_w[32];
+  level_ptr[0] = frames;
+  level_h[0] = h;
+  level_w[0] = w;
+  for (int l = 1; l < levels; ++l) {
+    level_h[l] = level_h[l - 1] / 2;
+    level_w[l] = level_w[l - 1] / 2;
+    level_buf[l] = reinterpret_cast<T*>(cur);
+    level_ptr[l] = level_buf[l];
+    cur += align256((size_t)nv * nf * level_h[l] * level_w[l] * sizeof(T));
+  }
+  T* dec_scratch = nullptr;
+  if (levels > 1) {
+    dec_scratch = reinterpret_cast<T*>(cur);
+    cur += align256((size_t)nv * nf * level_h[1] * level_w[1] * sizeof(T));
+  }
+  size_t mom = 0;
+  for (int l = 0; l < levels; ++l) mom = std::max(mom, moments_workspace(dt, nv, nf, level_h[l], level_w[l]));
+  void* mom_ws = cur;
+  for (int l = 0; l < levels; ++l) {
+    const bool next = l + 1 < levels;
+    int rc = moments_launch(dt, level_ptr[l], nv, nf, level_h[l], level_w[l], 1, sums + (size_t)l * np * 11, mom_ws,
+                            mom, st, next ? dec_scratch : nullptr);
+    if (rc) return rc;
+    if (next) {
+      rc = launch_blur_dec<T>(dec_scratch, nv * nf, level_h[l], level_w[l], level_buf[l + 1], st);
+      if (rc) return rc;
+    }
+  }
+  return CT_OK;
+}
+
 }  // namespace
 }  // namespace ct
 
@@ -903,4 +966,40 @@ extern "C" int ct_run_sequence(int dtype, const void* frames, int64_t n_videos, 
                            est, workspace, workspace_bytes, st);
   return run_seq<float>((const float*)frames, n_videos, (int)n_frames, (int)h, (int)w, level, max_level, c_min, est,
                         workspace, workspace_bytes, st);
+}
+
+static int check_pyr_args(int64_t n_frames, int64_t h, int64_t w, int levels) {
+  CT_REQUIRE(n_frames >= 2, "need at least two frames");
+  CT_REQUIRE(h < (1 << 30) && w < (1 << 30) && n_frames < (1 << 30), "extent too large");
+  CT_REQUIRE(levels >= 1 && levels < 31, "levels must be in [1, 30]");
+  int64_t lh = h, lw = w;
+  for (int i = 0; i < levels - 1; ++i) {
+    lh /= 2;
+    lw /= 2;
+  }
+  CT_REQUIRE(lh >= 4 && lw >= 4, "extents (%lld, %lld) leave (%lld, %lld) after %d halvings, need >= 4",
+             (long long)h, (long long)w, (long long)lh, (long long)lw, levels - 1);
+  return CT_OK;
+}
+
+extern "C" size_t ct_ttc_pyramid_moments_workspace_bytes(int dtype, int64_t n_videos, int64_t n_frames, int64_t h,
+                                                        int64_t w, int levels) {
+  if (n_frames < 2 || h < 1 || w < 1 || levels < 1 || levels > 30) return 0;
+  if (dtype == CT_F64) return pyr_ws<double>(n_videos, (int)n_frames, (int)h, (int)w, levels);
+  return pyr_ws<float>(n_videos, (int)n_frames, (int)h, (int)w, levels);
+}
+
+extern "C" int ct_ttc_pyramid_moments(int dtype, const void* frames, int64_t n_videos, int64_t n_frames, int64_t h,
+                                      int64_t w, int levels, double* sums, void* workspace, size_t workspace_bytes,
+                                      void* stream) {
+  clear_error();
+  CT_DT_CHECK(dtype);
+  int rc = check_pyr_args(n_frames, h, w, levels);
+  if (rc) return rc;
+  cudaStream_t st = as_stream(stream);
+  if (dtype == CT_F64)
+    return pyr_moments<double>((const double*)frames, n_videos, (int)n_frames, (int)h, (int)w, levels, sums,
+                               workspace, workspace_bytes, st);
+  return pyr_moments<float>((const float*)frames, n_videos, (int)n_frames, (int)h, (int)w, levels, sums, workspace,
+                            workspace_bytes, st);
 }

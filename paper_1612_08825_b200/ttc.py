@@ -218,6 +218,29 @@ def run_sequence_batch(frames, level: int | None = 0, max_level: int | None = No
     return out
 
 
+def pyramid_moments(frames, levels: int) -> torch.Tensor:
+    """Per-level normal-system sums of every consecutive frame pair on the
+    multiscale pyramid (ct_ttc_pyramid_moments): frames [V, n, h, w] CUDA
+    tensor -> [levels, V, n-1, 11] float64 (m00 m01 m02 m11 m12 m22, rhs0..2,
+    et2, count, as NormalSystem / build_normal_system, ttc.py:102-120).  Level l
+    is the l-fold downsample (ttc.py:187-204); these are the systems
+    estimate_multiscale solves level by level (ttc.py:248-279)."""
+    if not (isinstance(frames, torch.Tensor) and frames.is_cuda and frames.ndim == 4):
+        raise TypeError("pyramid_moments expects a CUDA tensor [V, n, h, w]")
+    f = frames.contiguous()
+    if f.dtype not in (torch.float32, torch.float64):
+        f = f.double()
+    V, n, h, w = f.shape
+    L = _lib.load()
+    dt = _lib.dtype_code(f)
+    nbytes = L.ct_ttc_pyramid_moments_workspace_bytes(dt, V, n, h, w, int(levels))
+    ws = _lib.workspace(nbytes, f.device)
+    out = torch.empty((int(levels), V, max(n - 1, 0), 11), dtype=torch.float64, device=f.device)
+    _lib.check(L.ct_ttc_pyramid_moments(dt, _lib.ptr(f), V, n, h, w, int(levels), _lib.ptr(out), _lib.ptr(ws),
+                                        nbytes, _lib.stream_ptr()))
+    return out
+
+
 def run_sequence_host(frames: np.ndarray, level: int | None = 0, max_level: int | None = None,
                       c_min: float = DEFAULT_C_MIN) -> np.ndarray:
     """run_sequence for a HOST stack [V, n, h, w] (float64 or float32 numpy, ideally

@@ -310,3 +310,28 @@ def test_randomized_shapes_levels_and_precisions():
         for v in range(nv):
             ref = O.run_sequence(f32[v].astype(np.float64), level=0)
             assert_est_close(got[v], ref, 1e-4, fields=(5,))
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_pyramid_moments_vs_oracle(dtype):
+    """ct_ttc_pyramid_moments: per-level sums equal the oracle's normal system
+    on the oracle's downsampled frames (fp64 1e-12 relative; fp32 frames 1e-5
+    against the fp64 reference of the rounded frames), and level 0 equals
+    ct_ttc_moments."""
+    f64 = O.generate(300, 140, 4, 80.0, (0.45, 0.5), 21, 0.0)
+    f = f64.astype(np.float32).astype(np.float64) if dtype == torch.float32 else f64
+    dev = torch.from_numpy(f).to(dtype).cuda()[None]
+    got = ct.pyramid_moments(dev, 3).cpu().numpy()
+    assert got.shape == (3, 1, 3, 11)
+    lv = [f[i] for i in range(4)]
+    tol = 1e-12 if dtype == torch.float64 else 1e-5
+    for level in range(3):
+        for i in range(3):
+            ex, ey, et = O.derivatives(lv[i], lv[i + 1])
+            ref = O.normal_system(ex, ey, O.radial_gradient(ex, ey), et, 1)
+            err = np.max(np.abs(got[level, 0, i, :10] - ref[:10])) / np.max(np.abs(ref[:10]))
+            assert err <= tol, (level, i, err)
+            assert got[level, 0, i, 10] == ref[10]
+        lv = [O.downsample(x) for x in lv]
+    with pytest.raises(ValueError, match="halvings"):
+        ct.pyramid_moments(dev, 7)
