@@ -18,6 +18,7 @@ arithmetic runs in libconvtact_b200.so (ct_direct); there is no CPU path.
 from __future__ import annotations
 
 import ctypes
+from collections import OrderedDict
 from dataclasses import dataclass
 from enum import Enum
 
@@ -95,6 +96,26 @@ def _host_kernel(kernel, dtype: torch.dtype) -> np.ndarray:
     return np.ascontiguousarray(kernel, dtype=np.float64 if dtype == torch.float64 else np.float32)
 
 
+_KD_CACHE: "OrderedDict[tuple, torch.Tensor]" = OrderedDict()
+
+
+def _device_kernel(k: np.ndarray, device: torch.device) -> torch.Tensor:
+    """Device copy of the taps (only the generic rank >= 4 kernel reads them;
+    the tiled kernels take the host copy through the parameter bank).  Cached
+    by content so repeated calls do no host->device copy (and can be captured
+    into a CUDA graph after a warm-up call)."""
+    key = (k.dtype.str, k.shape, k.tobytes(), device.index)
+    kd = _KD_CACHE.get(key)
+    if kd is None:
+        kd = torch.from_numpy(k).to(device)
+        _KD_CACHE[key] = kd
+        if len(_KD_CACHE) > 64:
+            _KD_CACHE.popitem(last=False)
+    else:
+        _KD_CACHE.move_to_end(key)
+    return kd
+
+
 def direct_batch(signals, kernel, shape=ConvShape.FULL, boundary=BoundaryPolicy.ZERO, flip=True,
                  out: torch.Tensor | None = None):
     """Batched direct conv/xcorr on the device: ``signals`` is [B, *extents].
@@ -114,7 +135,7 @@ def direct_batch(signals, kernel, shape=ConvShape.FULL, boundary=BoundaryPolicy.
     if out is None:
         out = torch.empty(oshape, dtype=s.dtype, device=s.device)
     L = _lib.load()
-    kd = torch.from_numpy(k).to(s.device)
+    kd = _device_kernel(k, s.device)
     rc = L.ct_direct(_lib.dtype_code(s), k.ndim, _lib.ptr(s), _lib.i64_array(s.shape[1:]), s.shape[0],
                      _lib.ptr(kd), k.ctypes.data_as(ctypes.c_void_p), _lib.i64_array(k.shape), _SHAPE[shape],
                      _BOUND[boundary], int(bool(flip)), _lib.ptr(out), _lib.stream_ptr())

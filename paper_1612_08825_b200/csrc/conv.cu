@@ -1650,7 +1650,12 @@ int run_tiled_autotuned(TileArgs a, int nw, bool is3d, const T* taps, int ntaps,
     for (const Variant& v : cands)
       if (v.kind == kind) return launch_variant<T>(a, v.kind, nw, is3d, v.txn, v.tyn, taps, ntaps, st);
   }
-  if (!tune || work < 2.0e8) return launch_variant<T>(a, cands[0].kind, nw, is3d, cands[0].txn, cands[0].tyn, taps, ntaps, st);
+  // timing candidates synchronises the stream: never while the stream is being
+  // captured into a CUDA graph (the cost-model pick is used instead)
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cap) != cudaSuccess) cudaGetLastError();
+  if (!tune || work < 2.0e8 || cap != cudaStreamCaptureStatusNone)
+    return launch_variant<T>(a, cands[0].kind, nw, is3d, cands[0].txn, cands[0].tyn, taps, ntaps, st);
 
   char key[256];
   snprintf(key, sizeof(key), "%zu|%d|%d,%d,%d|%d,%d,%d|%d,%d,%d|%d,%d,%d|%d|%lld", sizeof(T), nw, a.mz, a.my, a.mx,
@@ -1704,7 +1709,14 @@ int dispatch(int ndim, const void* s, const int64_t* ms, int64_t batch, const vo
   }
   if (o_elems == 0 || batch == 0) return CT_OK;
   const int nw = (int)ns[ndim - 1];
+  // the tiled kernels take the taps through the parameter bank; without a
+  // host copy that needs a device->host read, which cannot happen while the
+  // stream is captured into a CUDA graph (the generic kernel reads the taps
+  // from device memory instead)
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (!k_host && cudaStreamIsCapturing(st, &cap) != cudaSuccess) cudaGetLastError();
   const bool tiled_ok = ndim <= 3 && k_elems <= MaxTaps<T>::value && s_elems > 0 &&
+                        (k_host || cap == cudaStreamCaptureStatusNone) &&
                         (nw == 1 || nw == 2 || nw == 3 || nw == 4 || nw == 5 || nw == 6 ||
                          nw == 7 || nw == 8 || nw == 9 || nw == 11 || nw == 15 || nw == 31);
   if (tiled_ok) {

@@ -247,3 +247,24 @@ def test_each_3d_kernel_variant_matches_oracle(kind, monkeypatch):
         for i in range(2):
             ref = O.direct(s32[i].astype(np.float64), k32.astype(np.float64), shape.value, "zero", False)
             assert rel_inf(g32[i], ref) <= 1e-5, (kind, ms, ns)
+
+
+def test_cuda_graph_capture_replays_bit_identical():
+    """direct_batch can be captured into a CUDA graph after a warm-up call (no
+    host synchronisation or host->device copy on the launch path; the autotuner
+    never times candidates while the stream is capturing) and the replay equals
+    the eager result."""
+    rng = np.random.default_rng(5)
+    k = rng.standard_normal((5, 5))
+    s = torch.from_numpy(rng.random((64, 300, 260))).cuda()
+    eager = ct.direct_batch(s, k, F)
+    out = torch.empty_like(eager)
+    ct.direct_batch(s, k, F, out=out)  # warm-up: device taps cached, variant chosen
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        ct.direct_batch(s, k, F, out=out)
+    out.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, eager)
