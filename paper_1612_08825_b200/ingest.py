@@ -130,12 +130,13 @@ def load_pgm_frames(path) -> torch.Tensor:
         raise FormatError(f"{p}: no frame_*.pgm files")
     first, maxval = read_pgm_raw(files[0])
     pinned = torch.empty((len(files),) + first.shape, dtype=torch.uint8).pin_memory()
-    pinned[0].copy_(torch.from_numpy(np.ascontiguousarray(first)))
+    host = pinned.numpy()  # shares the pinned buffer; filled without wrapping read-only arrays
+    host[0] = first
     for i, f in enumerate(files[1:], start=1):
         raw, mv = read_pgm_raw(f)
         if raw.shape != first.shape or mv != maxval:
             raise FormatError(f"{f}: frame extents/maxval differ from {files[0].name}")
-        pinned[i].copy_(torch.from_numpy(np.ascontiguousarray(raw)))
+        host[i] = raw
     dev = pinned.to("cuda", non_blocking=True)
     h = first.shape[0]
     w = first.shape[1] // (2 if maxval == 65535 else 1)
