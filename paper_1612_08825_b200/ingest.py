@@ -114,7 +114,7 @@ def image_read_pgm(path):
     raw, maxval = read_pgm_raw(path)
     h = raw.shape[0]
     w = raw.shape[1] // (2 if maxval == 65535 else 1)
-    t = torch.from_numpy(np.ascontiguousarray(raw)).to("cuda")
+    t = torch.tensor(raw, device="cuda")  # copies (raw is a read-only view of the file bytes)
     return decode_on_device(t, maxval, (h, w)).cpu().numpy()
 
 
