@@ -569,6 +569,11 @@ constexpr int ring_buffers() {
   return sizeof(T) == 8 ? 3 : CT_MOM_NB32;
 }
 
+#ifndef CT_MOM_MIN_CHUNK
+#define CT_MOM_MIN_CHUNK 4
+#endif
+constexpr int kMinChunk = CT_MOM_MIN_CHUNK;  // fewest pairs per CTA chunk (each chunk re-reads one frame)
+
 struct Plan {
   int n_bands, n_ctiles, units, chunk, n_chunks, tile_cols;
 };
@@ -593,12 +598,12 @@ Plan make_plan(int64_t n_videos, int n_frames, int h, int w) {
   p.n_ctiles = (gw + p.tile_cols - 1) / p.tile_cols;
   p.units = p.n_bands * p.n_ctiles;
   const int n_pairs = n_frames - 1;
-  // ~4 waves of resident CTAs (2 per SM), but >= 8 pairs per CTA so the
+  // ~4 waves of resident CTAs (2 per SM), but >= kMinChunk pairs per CTA so the
   // one-frame time halo of each chunk stays small
   const int64_t target = (int64_t)num_sms() * (512 / BC) * 4;
   const int64_t per_chunk = std::max<int64_t>(1, (int64_t)p.units * n_videos);
   int64_t chunks = std::max<int64_t>(1, (target + per_chunk - 1) / per_chunk);
-  chunks = std::min<int64_t>(chunks, std::max(1, n_pairs / 8));
+  chunks = std::min<int64_t>(chunks, std::max(1, n_pairs / kMinChunk));
   chunks = std::max<int64_t>(1, std::min<int64_t>(chunks, n_pairs));
   p.chunk = (int)((n_pairs + chunks - 1) / chunks);
   p.n_chunks = (n_pairs + p.chunk - 1) / p.chunk;
