@@ -31,6 +31,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "common.cuh"
 #include "moments.cuh"
@@ -339,6 +340,241 @@ __device__ __forceinline__ void sweep_c2(const float* __restrict__ A, const floa
     m[c][7] = fmaf(K, L(s3), -L(q3));
     m[c][8] = fmaf(K, L(s5), -L(q5));
     m[c][9] = fmaf(K * K, L(s3), fmaf(-(2 * K + 1), L(q3), 2 * L(qq3)));
+  }
+}
+
+// This thread's ten normal-system sums for one pair (order m00 m01 m02 m11
+// m12 m22 r0 r1 r2 et2, rhs not yet negated) from its per-column sweep
+// sums: the band-relative y weights are shifted by the absolute centred y
+// of the thread's first row (yc0) and G = xc Ex + yc Ey is expanded with
+// the column's xc.
+template <typename ACC, int CPT, typename E>
+__device__ __forceinline__ void thread_sums(const ACC (&mc)[CPT][10], const bool (&in_col)[CPT],
+                                            const double (&xc)[CPT], double yc0d, E (&o)[10]) {
+  const E yc0 = (E)yc0d;  // centred coordinates are half-integers: exact in f32 and f64
+#pragma unroll
+  for (int q = 0; q < 10; ++q) o[q] = E(0);
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) {
+    if (in_col[c]) {
+      const ACC(&m)[10] = mc[c];
+      const E S1 = m[0], S2 = m[1], S3 = m[2], S4 = m[3], S5 = m[4], S6 = m[5];
+      const E U1 = fma(yc0, S2, (E)m[6]);
+      const E U2 = fma(yc0, S3, (E)m[7]);
+      const E U3 = fma(yc0, S5, (E)m[8]);
+      const E U4 = fma(yc0 * yc0, S3, fma(E(2) * yc0, (E)m[7], (E)m[9]));
+      const E X = (E)xc[c];
+      const E v[10] = {S1, S2, fma(X, S1, U1), S3, fma(X, S2, U2), fma(X * X, S1, fma(E(2) * X, U1, U4)),
+                       S4, S5, fma(X, S4, U3), S6};
+#pragma unroll
+      for (int q = 0; q < 10; ++q) o[q] = CPT == 1 ? v[q] : o[q] + v[q];
+    }
+  }
+}
+
+// Sum each of ten values over the 32 lanes of a warp with a fixed
+// transpose-reduce butterfly (10 -> 5 -> 3 -> 2 -> 1 values per lane over
+// xor 16, 8, 4, 2, 1; 12 shuffles and 12 adds per lane instead of 50).  On
+// return lane l holds the warp total of value `idx` (idx = -1: padding);
+// both lanes of an even/odd pair hold the same value.  The order of the adds
+// depends only on the lane, so the result is bit-reproducible.
+template <typename E>
+__device__ __forceinline__ E warp_reduce10(const E (&o)[10], int lane, int& idx) {
+  constexpr unsigned kFull = 0xffffffffu;
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
+  E r1[5];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    const E keep = b4 ? o[k + 5] : o[k], send = b4 ? o[k] : o[k + 5];
+    r1[k] = keep + __shfl_xor_sync(kFull, send, 16);
+  }
+  E r2[3];  // b3 = 0 keeps r1[0..2], b3 = 1 keeps r1[3..4] (+ padding)
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const E lo = r1[k], hi = k < 2 ? r1[3 + k] : E(0);
+    r2[k] = (b3 ? hi : lo) + __shfl_xor_sync(kFull, b3 ? lo : hi, 8);
+  }
+  E r3[2];  // b2 = 0 keeps r2[0..1], b2 = 1 keeps r2[2] (+ padding)
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const E lo = r2[k], hi = k < 1 ? r2[2] : E(0);
+    r3[k] = (b2 ? hi : lo) + __shfl_xor_sync(kFull, b2 ? lo : hi, 4);
+  }
+  const E r4 = (b1 ? r3[1] : r3[0]) + __shfl_xor_sync(kFull, b1 ? r3[0] : r3[1], 2);
+  const E r5 = r4 + __shfl_xor_sync(kFull, r4, 1);
+  // which value this lane ended with: list start/length after each split
+  int st = b4 ? 5 : 0, len = 5;
+  st += b3 ? 3 : 0;
+  len = b3 ? 2 : 3;
+  st += b2 ? 2 : 0;
+  len = b2 ? len - 2 : min(len, 2);
+  idx = (b1 ? len >= 2 : len >= 1) ? st + (b1 ? 1 : 0) : -1;
+  return r5;
+}
+
+template <typename T, int BR, int NB, int BC, int NT>
+struct SmemWS {  // warp-streaming kernel: NB frame-band buffers + per-buffer / per-pair counters + warp partials
+  static constexpr int NW = NT / 32;
+  static constexpr int NS = 3;  // pair slots for the warp partials (2 suffice, see the kernel)
+  static constexpr size_t buf_elems = (size_t)(BR + 1) * BC + 8;
+  static constexpr size_t buf_bytes = (buf_elems * sizeof(T) + 127) & ~size_t(127);
+  static constexpr size_t bars_off = NB * buf_bytes;
+  static constexpr size_t rel_off = bars_off + 8 * NB;
+  static constexpr size_t cnt_off = rel_off + 4 * NB;
+  static constexpr size_t part_off = (cnt_off + 4 * NS + 15) & ~size_t(15);
+  static constexpr size_t total = part_off + (size_t)NS * NW * 10 * sizeof(double);
+};
+
+// Warp-streaming variant of the fused moments kernel (used whenever the
+// frames admit a TMA map): no CTA-wide barrier in the steady state.
+//   * Each warp waits on the TMA mbarriers of the two frames of a pair by
+//     itself; when it has finished with frame i it bumps that buffer's
+//     release counter, and the last of the NW warps to release it issues the
+//     TMA of frame i + NB into the freed buffer.
+//   * A warp's 32 lanes reduce their ten sums with warp_reduce10 and deposit
+//     one 10-value partial per warp in a pair slot; the last warp to deposit
+//     for a pair adds the NW partials in warp order and writes the band's
+//     partial (same layout as the CTA-reduced kernel; the add order is fixed,
+//     so results stay bit-reproducible).
+//   * A warp can run at most NB - 1 pairs ahead of the slowest one (it waits
+//     for frame i + 1, which is only loaded once every warp released frame
+//     i + 1 - NB, after depositing for pair i + 1 - NB), so pair slot i % NS
+//     (NS >= 2) is never reused before its combine has run.
+//   * RS row splits: the 32 / RS lanes of a warp's row group own consecutive
+//     column groups (CPT columns each) and the RS groups split the band rows,
+//     so fp32 bands run 256 threads (16 warps per SM) with two columns per
+//     thread.
+template <typename T, int BR, int NB, int BC, int CPT, int RS>
+__global__ void __launch_bounds__(BC / CPT * RS, 512 / BC) ttc_moments_ws_kernel(const MomentArgs a,
+                                                                               const __grid_constant__ CUtensorMap tmap) {
+  using ACC = typename AccT<T>::type;
+  constexpr int kThreads = BC / CPT * RS;
+  using S = SmemWS<T, BR, NB, BC, kThreads>;
+  constexpr int NW = S::NW;
+  constexpr int HR = BR / RS;        // band rows per row group
+  constexpr int LG = 32 / RS;        // lanes per row group
+  static_assert(CPT == 1 || sizeof(T) == 4, "two columns per thread is the fp32 path");
+  static_assert(BR % RS == 0 && 32 % RS == 0, "row split");
+  extern __shared__ __align__(128) unsigned char smem[];
+  auto buf = [&](int k) { return reinterpret_cast<T*>(smem + (size_t)k * S::buf_bytes); };
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::bars_off);
+  int* rel = reinterpret_cast<int*>(smem + S::rel_off);
+  int* cnt = reinterpret_cast<int*>(smem + S::cnt_off);
+  double* part = reinterpret_cast<double*>(smem + S::part_off);
+
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int unit = blockIdx.x;
+  const int band = unit / a.n_ctiles, ctile = unit - band * a.n_ctiles;
+  const int gy0 = band * BR;
+  const int cx0 = ctile * a.tile_cols;
+  const int64_t v = blockIdx.z;
+  const int n_pairs = a.n_frames - 1;
+  const int p0 = blockIdx.y * a.chunk;
+  const int p1 = min(p0 + a.chunk, n_pairs);
+  if (p0 >= p1) return;
+  const int nload = p1 - p0 + 1;
+  constexpr uint32_t kBoxBytes = (uint32_t)((BR + 1) * BC * sizeof(T));
+
+  const int rg = lane / LG;                              // row group of this lane
+  const int col = (wid * LG + lane % LG) * CPT;           // first tile column of this thread
+  const int r0 = rg * HR;                                 // rows r0+1 .. r0+HR of the band (start row r0)
+  bool in_col[CPT];
+  double xc[CPT];
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) {
+    const int gx = cx0 + col + c;
+    in_col[c] = col + c < a.tile_cols && gx >= a.border && gx < a.gw - a.border;
+    xc[c] = (double)gx - (double)(a.gw - 1) / 2.0;
+  }
+  const double yc0 = (double)(gy0 + r0) - (double)(a.gh - 1) / 2.0;  // centred y of this thread's first grid row
+  const int64_t row0 = (v * a.n_frames) * (int64_t)a.h + gy0;
+  // thread-local row range [r_beg, r_end] (1..HR) whose grid rows are interior
+  const int r_end = min(HR, a.gh - a.border - gy0 - r0);
+  const int r_beg = max(1, a.border - gy0 - r0 + 1);
+
+  auto issue = [&](int f) {
+    fence_proxy_async_smem();
+    mbar_arrive_expect_tx(&bars[f % NB], kBoxBytes);
+    tma_load_2d(buf(f % NB), &tmap, &bars[f % NB], cx0, (int)(row0 + (int64_t)(p0 + f) * a.h));
+  };
+  if (tid == 0) {
+    for (int i = 0; i < NB; ++i) {
+      mbar_init(&bars[i], 1);
+      rel[i] = 0;
+    }
+    for (int i = 0; i < S::NS; ++i) cnt[i] = 0;
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int f = 0; f < min(NB, nload); ++f) issue(f);
+
+  for (int i = 0; i < p1 - p0; ++i) {
+    const int p = p0 + i;
+    mbar_wait(&bars[i % NB], (uint32_t)((i / NB) & 1));
+    mbar_wait(&bars[(i + 1) % NB], (uint32_t)(((i + 1) / NB) & 1));
+    const T* A = buf(i % NB);
+    const T* B = buf((i + 1) % NB);
+    if (a.dec) {
+      write_dec<T, BR, kThreads, BC>(a, A, v, p, gy0, cx0, tid);
+      if (p1 == n_pairs && i == p1 - p0 - 1) write_dec<T, BR, kThreads, BC>(a, B, v, p1, gy0, cx0, tid);
+    }
+    const T* Ar = A + r0 * BC;
+    const T* Br = B + r0 * BC;
+    ACC mc[CPT][10];
+    if constexpr (CPT == 2) {
+      if (r_beg <= 1 && r_end >= HR)
+        sweep_c2<HR, false, BC>(reinterpret_cast<const float*>(Ar), reinterpret_cast<const float*>(Br), col, 1, HR,
+                                mc);
+      else
+        sweep_c2<HR, true, BC>(reinterpret_cast<const float*>(Ar), reinterpret_cast<const float*>(Br), col, r_beg,
+                               r_end, mc);
+    } else {
+      ACC(&m)[10] = mc[0];
+      if (r_beg <= 1 && r_end >= HR) {
+        if constexpr (sizeof(T) == 4 && kPackedF32 && HR % 2 == 0)
+          sweep_x2<HR, BC>(reinterpret_cast<const float*>(Ar), reinterpret_cast<const float*>(Br), col, m);
+        else
+          sweep<T, HR, false, BC>(Ar, Br, col, 1, HR, m);
+      } else {
+        sweep<T, HR, true, BC>(Ar, Br, col, r_beg, r_end, m);
+      }
+    }
+    // fp32 frames: per-thread epilogue and warp reduction in fp32 (the FP64
+    // pipe is half rate); fp64 frames: fp64 throughout
+    using E = typename std::conditional<sizeof(T) == 4, float, double>::type;
+    E o[10];
+    thread_sums<ACC, CPT, E>(mc, in_col, xc, yc0, o);
+    int idx;
+    const double wsum = (double)warp_reduce10<E>(o, lane, idx);
+    const int slot = i % S::NS;
+    double* ps = part + (size_t)slot * NW * 10;
+    if ((lane & 1) == 0 && idx >= 0) ps[wid * 10 + idx] = wsum;
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) {
+      __threadfence_block();
+      last = (atomicAdd(&cnt[slot], 1) % NW) == NW - 1;
+      if (last) __threadfence_block();
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last) {  // every warp has deposited for pair p: add the partials in warp order
+      __syncwarp();
+      if (lane < 10) {
+        double acc = 0.0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) acc += ps[w * 10 + lane];
+        acc *= 0.0625;  // undo the 4x stencil scaling of both factors
+        a.partials[((v * n_pairs + p) * a.units + unit) * 10 + lane] = (lane >= 6 && lane <= 8) ? -acc : acc;
+      }
+    }
+    __syncwarp();
+    // frame p0 + i (buffer i % NB) is dead for this warp: the last warp to
+    // release it refills the buffer with frame p0 + i + NB
+    if (lane == 0) {
+      __threadfence_block();
+      if ((atomicAdd(&rel[i % NB], 1) % NW) == NW - 1 && i + NB < nload) issue(i + NB);
+    }
   }
 }
 
@@ -655,11 +891,28 @@ int launch_bc(const T* frames, int64_t n_videos, int n_frames, int h, int w, int
                                         (uint64_t)(n_videos * n_frames * (int64_t)h), BC, BR + 1);
   constexpr int NB = ring_buffers<T>();
   constexpr int CPT = (sizeof(T) == 4 && kTwoColF32 && BC == 256) ? 2 : 1;
-  using S = Smem<T, BR, NB, BC, BC / CPT>;
-  auto kern = ttc_moments_kernel<T, BR, NB, BC, CPT>;
-  CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::total));
   dim3 grid((unsigned)p.units, (unsigned)p.n_chunks, (unsigned)n_videos);
-  kern<<<grid, BC / CPT, S::total, st>>>(a, tmap);
+  static const bool sync_kernel = getenv("CT_MOM_SYNC") != nullptr;  // probing: the CTA-barrier kernel
+  static const int rs_env = getenv("CT_MOM_RS") ? atoi(getenv("CT_MOM_RS")) : 1;  // probing: fp32 row split
+  if (a.use_tma && !sync_kernel) {
+    if (CPT == 2 && rs_env == 2) {
+      constexpr int RS = CPT == 2 ? 2 : 1;
+      using S = SmemWS<T, BR, NB, BC, BC / CPT * RS>;
+      auto kern = ttc_moments_ws_kernel<T, BR, NB, BC, CPT, RS>;
+      CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::total));
+      kern<<<grid, BC / CPT * RS, S::total, st>>>(a, tmap);
+    } else {
+      using S = SmemWS<T, BR, NB, BC, BC / CPT>;
+      auto kern = ttc_moments_ws_kernel<T, BR, NB, BC, CPT, 1>;
+      CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::total));
+      kern<<<grid, BC / CPT, S::total, st>>>(a, tmap);
+    }
+  } else {
+    using S = Smem<T, BR, NB, BC, BC / CPT>;
+    auto kern = ttc_moments_kernel<T, BR, NB, BC, CPT>;
+    CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::total));
+    kern<<<grid, BC / CPT, S::total, st>>>(a, tmap);
+  }
   int rc = check_launch("ttc_moments");
   if (rc) return rc;
   const int64_t n_sys = n_videos * n_pairs;
