@@ -133,7 +133,10 @@ struct Smem {  // NB = frame-band buffers in the TMA ring (NB - 2 frames in flig
 // four adds per row replace one multiply and four FMAs.  Rows outside
 // [r_beg, r_end] leave S unchanged (t_r = 0) but still advance Q and QQ.
 // CHECK=false is the interior fast path (all rows, no per-row tests).
-template <typename T, int BR, bool CHECK, int BC>
+// RAW = true returns the running sums themselves in m[6..9] (Q2, Q3, Q5, QQ3);
+// thread_sums<RAW> then folds the band-relative weights and the absolute
+// shift into one step (three FP64 operations fewer per pair).
+template <typename T, int BR, bool CHECK, int BC, bool RAW = false>
 __device__ __forceinline__ void sweep(const T* __restrict__ A, const T* __restrict__ B, int col, int r_beg,
                                       int r_end, typename AccT<T>::type (&m)[10]) {
   using ACC = typename AccT<T>::type;
@@ -181,10 +184,14 @@ __device__ __forceinline__ void sweep(const T* __restrict__ A, const T* __restri
   }
   constexpr ACC K = ACC(BR);
   m[0] = s1; m[1] = s2; m[2] = s3; m[3] = s4; m[4] = s5; m[5] = s6;
-  m[6] = fma(K, s2, -q2);
-  m[7] = fma(K, s3, -q3);
-  m[8] = fma(K, s5, -q5);
-  m[9] = fma(K * K, s3, fma(-(2 * K + 1), q3, 2 * qq3));
+  if constexpr (RAW) {
+    m[6] = q2; m[7] = q3; m[8] = q5; m[9] = qq3;
+  } else {
+    m[6] = fma(K, s2, -q2);
+    m[7] = fma(K, s3, -q3);
+    m[8] = fma(K, s5, -q5);
+    m[9] = fma(K * K, s3, fma(-(2 * K + 1), q3, 2 * qq3));
+  }
 }
 
 // fp32 interior sweep with packed f32x2 arithmetic: lane .x of every pair
@@ -348,10 +355,14 @@ __device__ __forceinline__ void sweep_c2(const float* __restrict__ A, const floa
 // sums: the band-relative y weights are shifted by the absolute centred y
 // of the thread's first row (yc0) and G = xc Ex + yc Ey is expanded with
 // the column's xc.
-template <typename ACC, int CPT, typename E>
+// RAW: m[6..9] are the running sums (Q2, Q3, Q5, QQ3) of a K-row sweep; with
+// Y = yc0 + K, U1 = Y S2 - Q2, U2 = Y S3 - Q3, U3 = Y S5 - Q5 and
+// U4 = Y^2 S3 - (2Y + 1) Q3 + 2 QQ3 (sweep()'s identities with the shift folded in).
+template <typename ACC, int CPT, typename E, bool RAW = false, int K = 0>
 __device__ __forceinline__ void thread_sums(const ACC (&mc)[CPT][10], const bool (&in_col)[CPT],
                                             const double (&xc)[CPT], double yc0d, E (&o)[10]) {
   const E yc0 = (E)yc0d;  // centred coordinates are half-integers: exact in f32 and f64
+  const E Y = yc0 + E(K);
 #pragma unroll
   for (int q = 0; q < 10; ++q) o[q] = E(0);
 #pragma unroll
@@ -359,10 +370,18 @@ __device__ __forceinline__ void thread_sums(const ACC (&mc)[CPT][10], const bool
     if (in_col[c]) {
       const ACC(&m)[10] = mc[c];
       const E S1 = m[0], S2 = m[1], S3 = m[2], S4 = m[3], S5 = m[4], S6 = m[5];
-      const E U1 = fma(yc0, S2, (E)m[6]);
-      const E U2 = fma(yc0, S3, (E)m[7]);
-      const E U3 = fma(yc0, S5, (E)m[8]);
-      const E U4 = fma(yc0 * yc0, S3, fma(E(2) * yc0, (E)m[7], (E)m[9]));
+      E U1, U2, U3, U4;
+      if constexpr (RAW) {
+        U1 = fma(Y, S2, -(E)m[6]);
+        U2 = fma(Y, S3, -(E)m[7]);
+        U3 = fma(Y, S5, -(E)m[8]);
+        U4 = fma(Y * Y, S3, fma(-(E(2) * Y + E(1)), (E)m[7], (E)m[9] + (E)m[9]));
+      } else {
+        U1 = fma(yc0, S2, (E)m[6]);
+        U2 = fma(yc0, S3, (E)m[7]);
+        U3 = fma(yc0, S5, (E)m[8]);
+        U4 = fma(yc0 * yc0, S3, fma(E(2) * yc0, (E)m[7], (E)m[9]));
+      }
       const E X = (E)xc[c];
       const E v[10] = {S1, S2, fma(X, S1, U1), S3, fma(X, S2, U2), fma(X * X, S1, fma(E(2) * X, U1, U4)),
                        S4, S5, fma(X, S4, U3), S6};
@@ -444,9 +463,18 @@ struct SmemWS {  // warp-streaming kernel: NB frame-band buffers + per-buffer / 
 //     column groups (CPT columns each) and the RS groups split the band rows,
 //     so fp32 bands run 256 threads (16 warps per SM) with two columns per
 //     thread.
+#ifndef CT_MOM_MINB32
+#define CT_MOM_MINB32 0
+#endif
+// resident CTAs per SM the register budget is sized for (fp32 probing: CT_MOM_MINB32)
+template <typename T, int BC, int RS>
+constexpr int ws_min_blocks() {
+  return (sizeof(T) == 4 && CT_MOM_MINB32 > 0) ? CT_MOM_MINB32 : ((512 / BC) / RS > 0 ? (512 / BC) / RS : 1);
+}
+
 template <typename T, int BR, int NB, int BC, int CPT, int RS>
-__global__ void __launch_bounds__(BC / CPT * RS, 512 / BC) ttc_moments_ws_kernel(const MomentArgs a,
-                                                                               const __grid_constant__ CUtensorMap tmap) {
+__device__ __forceinline__ void moments_ws_body(const MomentArgs& a, const CUtensorMap* tmap, unsigned char* smem,
+                                                int unit, int chunk_idx, int64_t v) {
   using ACC = typename AccT<T>::type;
   constexpr int kThreads = BC / CPT * RS;
   using S = SmemWS<T, BR, NB, BC, kThreads>;
@@ -455,7 +483,8 @@ __global__ void __launch_bounds__(BC / CPT * RS, 512 / BC) ttc_moments_ws_kernel
   constexpr int LG = 32 / RS;        // lanes per row group
   static_assert(CPT == 1 || sizeof(T) == 4, "two columns per thread is the fp32 path");
   static_assert(BR % RS == 0 && 32 % RS == 0, "row split");
-  extern __shared__ __align__(128) unsigned char smem[];
+  // fp64 single-column sweeps hand back raw running sums (folded in thread_sums)
+  constexpr bool kRaw = sizeof(T) == 8 && CPT == 1;
   auto buf = [&](int k) { return reinterpret_cast<T*>(smem + (size_t)k * S::buf_bytes); };
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::bars_off);
   int* rel = reinterpret_cast<int*>(smem + S::rel_off);
@@ -463,13 +492,11 @@ __global__ void __launch_bounds__(BC / CPT * RS, 512 / BC) ttc_moments_ws_kernel
   double* part = reinterpret_cast<double*>(smem + S::part_off);
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int unit = blockIdx.x;
   const int band = unit / a.n_ctiles, ctile = unit - band * a.n_ctiles;
   const int gy0 = band * BR;
   const int cx0 = ctile * a.tile_cols;
-  const int64_t v = blockIdx.z;
   const int n_pairs = a.n_frames - 1;
-  const int p0 = blockIdx.y * a.chunk;
+  const int p0 = chunk_idx * a.chunk;
   const int p1 = min(p0 + a.chunk, n_pairs);
   if (p0 >= p1) return;
   const int nload = p1 - p0 + 1;
@@ -495,7 +522,7 @@ __global__ void __launch_bounds__(BC / CPT * RS, 512 / BC) ttc_moments_ws_kernel
   auto issue = [&](int f) {
     fence_proxy_async_smem();
     mbar_arrive_expect_tx(&bars[f % NB], kBoxBytes);
-    tma_load_2d(buf(f % NB), &tmap, &bars[f % NB], cx0, (int)(row0 + (int64_t)(p0 + f) * a.h));
+    tma_load_2d(buf(f % NB), tmap, &bars[f % NB], cx0, (int)(row0 + (int64_t)(p0 + f) * a.h));
   };
   if (tid == 0) {
     for (int i = 0; i < NB; ++i) {
@@ -535,16 +562,16 @@ __global__ void __launch_bounds__(BC / CPT * RS, 512 / BC) ttc_moments_ws_kernel
         if constexpr (sizeof(T) == 4 && kPackedF32 && HR % 2 == 0)
           sweep_x2<HR, BC>(reinterpret_cast<const float*>(Ar), reinterpret_cast<const float*>(Br), col, m);
         else
-          sweep<T, HR, false, BC>(Ar, Br, col, 1, HR, m);
+          sweep<T, HR, false, BC, kRaw>(Ar, Br, col, 1, HR, m);
       } else {
-        sweep<T, HR, true, BC>(Ar, Br, col, r_beg, r_end, m);
+        sweep<T, HR, true, BC, kRaw>(Ar, Br, col, r_beg, r_end, m);
       }
     }
     // fp32 frames: per-thread epilogue and warp reduction in fp32 (the FP64
     // pipe is half rate); fp64 frames: fp64 throughout
     using E = typename std::conditional<sizeof(T) == 4, float, double>::type;
     E o[10];
-    thread_sums<ACC, CPT, E>(mc, in_col, xc, yc0, o);
+    thread_sums<ACC, CPT, E, kRaw, HR>(mc, in_col, xc, yc0, o);
     int idx;
     const double wsum = (double)warp_reduce10<E>(o, lane, idx);
     const int slot = i % S::NS;
@@ -576,6 +603,38 @@ __global__ void __launch_bounds__(BC / CPT * RS, 512 / BC) ttc_moments_ws_kernel
       if ((atomicAdd(&rel[i % NB], 1) % NW) == NW - 1 && i + NB < nload) issue(i + NB);
     }
   }
+}
+
+template <typename T, int BR, int NB, int BC, int CPT, int RS>
+__global__ void __launch_bounds__(BC / CPT * RS, ws_min_blocks<T, BC, RS>())
+    ttc_moments_ws_kernel(const MomentArgs a, const __grid_constant__ CUtensorMap tmap) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  moments_ws_body<T, BR, NB, BC, CPT, RS>(a, &tmap, smem, blockIdx.x, blockIdx.y, blockIdx.z);
+}
+
+// Several pyramid levels in one launch (the small levels alone cannot fill
+// the GPU): a 1-D grid whose CTAs are the concatenated (unit, chunk, video)
+// grids of the levels, largest level first.
+constexpr int kMaxLevels = kMomentLevelsPerLaunch;
+struct LevelsArgs {
+  CUtensorMap tmap[kMaxLevels];
+  MomentArgs a[kMaxLevels];
+  int64_t cta_end[kMaxLevels];
+  int n;
+};
+
+template <typename T, int BR, int NB, int BC, int CPT, int RS>
+__global__ void __launch_bounds__(BC / CPT * RS, ws_min_blocks<T, BC, RS>())
+    ttc_moments_levels_kernel(const __grid_constant__ LevelsArgs m) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  int l = 0;
+  while (l + 1 < m.n && (int64_t)blockIdx.x >= m.cta_end[l]) ++l;
+  const int64_t local = (int64_t)blockIdx.x - (l ? m.cta_end[l - 1] : 0);
+  const MomentArgs& a = m.a[l];
+  const int unit = (int)(local % a.units);
+  const int64_t rest = local / a.units;
+  const int n_chunks = (a.n_frames - 1 + a.chunk - 1) / a.chunk;
+  moments_ws_body<T, BR, NB, BC, CPT, RS>(a, &m.tmap[l], smem, unit, (int)(rest % n_chunks), rest / n_chunks);
 }
 
 template <typename T, int BR, int NB, int BC, int CPT>
@@ -796,13 +855,19 @@ inline unsigned finalize_grid(int64_t n_sys) {
 #ifndef CT_MOM_NB32
 #define CT_MOM_NB32 3
 #endif
+#ifndef CT_MOM_BR64
+#define CT_MOM_BR64 16
+#endif
+#ifndef CT_MOM_NB64
+#define CT_MOM_NB64 3
+#endif
 template <typename T>
 constexpr int band_rows() {
-  return sizeof(T) == 8 ? 16 : CT_MOM_BR32;
+  return sizeof(T) == 8 ? CT_MOM_BR64 : CT_MOM_BR32;
 }
 template <typename T>
 constexpr int ring_buffers() {
-  return sizeof(T) == 8 ? 3 : CT_MOM_NB32;
+  return sizeof(T) == 8 ? CT_MOM_NB64 : CT_MOM_NB32;
 }
 
 #ifndef CT_MOM_MIN_CHUNK
@@ -859,17 +924,20 @@ size_t ws_bytes(int64_t n_videos, int n_frames, int h, int w) {
 }
 
 template <typename T, int BC>
-int launch_bc(const T* frames, int64_t n_videos, int n_frames, int h, int w, int border, double* sums, void* ws,
-              size_t ws_size, void* dec, cudaStream_t st) {
-  const int n_pairs = n_frames - 1;
+constexpr int cols_per_thread() {
+  return (sizeof(T) == 4 && kTwoColF32 && BC == 256) ? 2 : 1;
+}
+
+// Kernel arguments and TMA map of one level; returns whether the frames admit
+// a TMA map (16-byte aligned base and row pitch), else the LDG-loader kernel runs.
+template <typename T, int BC>
+bool prep_level(MomentArgs& a, CUtensorMap& tmap, const T* frames, int64_t n_videos, int n_frames, int h, int w,
+                int border, double* partials, void* dec) {
   constexpr int BR = band_rows<T>();
   const Plan p = make_plan<T, BC>(n_videos, n_frames, h, w);
-  const size_t need = ws_bytes<T>(n_videos, n_frames, h, w);
-  CT_REQUIRE(ws != nullptr && ws_size >= need, "moments workspace too small (%zu < %zu)", ws_size, need);
-  CT_REQUIRE(n_videos <= 65535 && p.n_chunks <= 65535, "too many videos/chunks for one launch");
-  MomentArgs a{};
+  a = MomentArgs{};
   a.frames = frames;
-  a.partials = reinterpret_cast<double*>(ws);
+  a.partials = partials;
   a.n_videos = n_videos;
   a.n_frames = n_frames;
   a.h = h;
@@ -884,40 +952,50 @@ int launch_bc(const T* frames, int64_t n_videos, int n_frames, int h, int w, int
   a.dec = dec;
   a.dh = h / 2;
   a.dw = w / 2;
-  CUtensorMap tmap;
   memset(&tmap, 0, sizeof(tmap));
   static const bool no_tma = getenv("CT_NO_TMA") != nullptr;  // debugging switch: force the LDG loader
   a.use_tma = !no_tma && encode_tmap_2d(&tmap, frames, sizeof(T), (uint64_t)w,
                                         (uint64_t)(n_videos * n_frames * (int64_t)h), BC, BR + 1);
+  return a.use_tma;
+}
+
+// Band partials of one level (no finalize).
+template <typename T, int BC>
+int launch_partials(const MomentArgs& a, const CUtensorMap& tmap, cudaStream_t st) {
+  constexpr int BR = band_rows<T>();
   constexpr int NB = ring_buffers<T>();
-  constexpr int CPT = (sizeof(T) == 4 && kTwoColF32 && BC == 256) ? 2 : 1;
-  dim3 grid((unsigned)p.units, (unsigned)p.n_chunks, (unsigned)n_videos);
+  constexpr int CPT = cols_per_thread<T, BC>();
+  const int n_chunks = (a.n_frames - 1 + a.chunk - 1) / a.chunk;
+  CT_REQUIRE(a.n_videos <= 65535 && n_chunks <= 65535, "too many videos/chunks for one launch");
+  dim3 grid((unsigned)a.units, (unsigned)n_chunks, (unsigned)a.n_videos);
   static const bool sync_kernel = getenv("CT_MOM_SYNC") != nullptr;  // probing: the CTA-barrier kernel
-  static const int rs_env = getenv("CT_MOM_RS") ? atoi(getenv("CT_MOM_RS")) : 1;  // probing: fp32 row split
   if (a.use_tma && !sync_kernel) {
-    if (CPT == 2 && rs_env == 2) {
-      constexpr int RS = CPT == 2 ? 2 : 1;
-      using S = SmemWS<T, BR, NB, BC, BC / CPT * RS>;
-      auto kern = ttc_moments_ws_kernel<T, BR, NB, BC, CPT, RS>;
-      CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::total));
-      kern<<<grid, BC / CPT * RS, S::total, st>>>(a, tmap);
-    } else {
-      using S = SmemWS<T, BR, NB, BC, BC / CPT>;
-      auto kern = ttc_moments_ws_kernel<T, BR, NB, BC, CPT, 1>;
-      CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::total));
-      kern<<<grid, BC / CPT, S::total, st>>>(a, tmap);
-    }
+    using S = SmemWS<T, BR, NB, BC, BC / CPT>;
+    auto kern = ttc_moments_ws_kernel<T, BR, NB, BC, CPT, 1>;
+    CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::total));
+    kern<<<grid, BC / CPT, S::total, st>>>(a, tmap);
   } else {
     using S = Smem<T, BR, NB, BC, BC / CPT>;
     auto kern = ttc_moments_kernel<T, BR, NB, BC, CPT>;
     CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::total));
     kern<<<grid, BC / CPT, S::total, st>>>(a, tmap);
   }
-  int rc = check_launch("ttc_moments");
+  return check_launch("ttc_moments");
+}
+
+template <typename T, int BC>
+int launch_bc(const T* frames, int64_t n_videos, int n_frames, int h, int w, int border, double* sums, void* ws,
+              size_t ws_size, void* dec, cudaStream_t st) {
+  const size_t need = ws_bytes<T>(n_videos, n_frames, h, w);
+  CT_REQUIRE(ws != nullptr && ws_size >= need, "moments workspace too small (%zu < %zu)", ws_size, need);
+  MomentArgs a;
+  CUtensorMap tmap;
+  prep_level<T, BC>(a, tmap, frames, n_videos, n_frames, h, w, border, reinterpret_cast<double*>(ws), dec);
+  int rc = launch_partials<T, BC>(a, tmap, st);
   if (rc) return rc;
-  const int64_t n_sys = n_videos * n_pairs;
+  const int64_t n_sys = n_videos * (n_frames - 1);
   const double count = (double)(h - 1 - 2 * border) * (double)(w - 1 - 2 * border);
-  moments_finalize_kernel<<<finalize_grid(n_sys), kFinWarps * 32, 0, st>>>(a.partials, n_sys, p.units, count, sums);
+  moments_finalize_kernel<<<finalize_grid(n_sys), kFinWarps * 32, 0, st>>>(a.partials, n_sys, a.units, count, sums);
   return check_launch("moments_finalize");
 }
 
@@ -927,6 +1005,40 @@ int launch(const T* frames, int64_t n_videos, int n_frames, int h, int w, int bo
   if (n_frames - 1 <= 0 || n_videos == 0) return CT_OK;
   if (pick_bc(w) == 128) return launch_bc<T, 128>(frames, n_videos, n_frames, h, w, border, sums, ws, ws_size, dec, st);
   return launch_bc<T, 256>(frames, n_videos, n_frames, h, w, border, sums, ws, ws_size, dec, st);
+}
+
+// Band partials of several levels: one launch of the levels kernel when every
+// level has a TMA map, else one launch per level.
+template <typename T, int BC>
+int launch_levels_bc(const MomentLevel* lv, int n, int64_t n_videos, int n_frames, int border, cudaStream_t st) {
+  CT_REQUIRE(n >= 1 && n <= kMaxLevels, "1..%d levels per launch", kMaxLevels);
+  LevelsArgs m;
+  memset(&m, 0, sizeof(m));
+  m.n = n;
+  bool all_tma = getenv("CT_MOM_SYNC") == nullptr;
+  int64_t ctas = 0;
+  for (int l = 0; l < n; ++l) {
+    all_tma &= prep_level<T, BC>(m.a[l], m.tmap[l], reinterpret_cast<const T*>(lv[l].frames), n_videos, n_frames,
+                                 lv[l].h, lv[l].w, border, lv[l].partials, lv[l].dec);
+    const int n_chunks = (n_frames - 1 + m.a[l].chunk - 1) / m.a[l].chunk;
+    ctas += (int64_t)m.a[l].units * n_chunks * n_videos;
+    m.cta_end[l] = ctas;
+  }
+  if (n == 1 || !all_tma || ctas > 0x7fffffffll) {
+    for (int l = 0; l < n; ++l) {
+      int rc = launch_partials<T, BC>(m.a[l], m.tmap[l], st);
+      if (rc) return rc;
+    }
+    return CT_OK;
+  }
+  constexpr int BR = band_rows<T>();
+  constexpr int NB = ring_buffers<T>();
+  constexpr int CPT = cols_per_thread<T, BC>();
+  using S = SmemWS<T, BR, NB, BC, BC / CPT>;
+  auto kern = ttc_moments_levels_kernel<T, BR, NB, BC, CPT, 1>;
+  CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::total));
+  kern<<<(unsigned)ctas, BC / CPT, S::total, st>>>(m);
+  return check_launch("ttc_moments_levels");
 }
 
 }  // namespace
@@ -940,6 +1052,22 @@ int moments_launch(int dtype, const void* frames, int64_t n_videos, int n_frames
   if (dtype == CT_F64)
     return launch<double>((const double*)frames, n_videos, n_frames, h, w, border, sums, ws, ws_size, dec, st);
   return launch<float>((const float*)frames, n_videos, n_frames, h, w, border, sums, ws, ws_size, dec, st);
+}
+
+int moments_units(int dtype, int64_t n_videos, int n_frames, int h, int w) {
+  return dtype == CT_F64 ? make_plan<double>(n_videos, n_frames, h, w).units
+                         : make_plan<float>(n_videos, n_frames, h, w).units;
+}
+
+int moments_levels_launch(int dtype, const MomentLevel* lv, int n_levels, int64_t n_videos, int n_frames, int border,
+                          cudaStream_t st) {
+  if (n_frames - 1 <= 0 || n_videos == 0 || n_levels == 0) return CT_OK;
+  const int w0 = lv[0].w;
+  if (dtype == CT_F64)
+    return pick_bc(w0) == 128 ? launch_levels_bc<double, 128>(lv, n_levels, n_videos, n_frames, border, st)
+                              : launch_levels_bc<double, 256>(lv, n_levels, n_videos, n_frames, border, st);
+  return pick_bc(w0) == 128 ? launch_levels_bc<float, 128>(lv, n_levels, n_videos, n_frames, border, st)
+                            : launch_levels_bc<float, 256>(lv, n_levels, n_videos, n_frames, border, st);
 }
 
 int partials_finalize(const double* partials, int64_t n_sys, int units, double count, double* sums,

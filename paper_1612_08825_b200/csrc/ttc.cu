@@ -491,7 +491,7 @@ constexpr int kBlurRch = 4, kBlurStages = 4, kBlurWarps = 8;
 template <typename T>
 __global__ void __launch_bounds__(kBlurWarps * 32) blur5_tma_kernel(const __grid_constant__ CUtensorMap tmap,
                                                                      int64_t n_images, int dh, int dw, int strip,
-                                                                     T* __restrict__ out) {
+                                                                     T* __restrict__ out, T* __restrict__ dec_out) {
   constexpr int VX = 16 / sizeof(T);
   constexpr int SC = 32 * VX + 2 * VX;  // staged columns per row: slab + VX each side (16-byte aligned)
   constexpr int STAGE = kBlurRch * SC;  // elements per stage
@@ -536,6 +536,7 @@ __global__ void __launch_bounds__(kBlurWarps * 32) blur5_tma_kernel(const __grid
     for (int c = 0; c < kBlurStages && c < nchunks; ++c) issue(c);
     T h[5][VX];
     T hcur[VX];
+    T prev[VX];     // previous output row (the even row of a 2x2 block for dec_out)
     int have = -1;  // image row whose horizontal sums are in hcur
     for (int yy = y0 - 2; yy < y1 + 2; ++yy) {
       const int r = min(max(yy, 0), dh - 1);
@@ -587,6 +588,25 @@ __global__ void __launch_bounds__(kBlurWarps * 32) blur5_tma_kernel(const __grid
           ov[cc] = acc;
         }
         *reinterpret_cast<V*>(out + (img * (int64_t)dh + (yy - 2)) * dw + x) = o;
+        // next level's 2x2 block means (ttc.py:202-203 on this level's even
+        // crop), same add order as write_dec: ((p00 + p01) + p10) + p11
+        const int y = yy - 2, ddh = dh >> 1, ddw = dw >> 1;
+        if (dec_out != nullptr && (y & 1) && (y >> 1) < ddh) {
+#pragma unroll
+          for (int k = 0; k < VX / 2; ++k) {
+            const int xd = (x >> 1) + k;
+            if (xd < ddw) {
+              T d;
+              if constexpr (sizeof(T) == 8)
+                d = __dmul_rn(0.25, __dadd_rn(__dadd_rn(__dadd_rn(prev[2 * k], prev[2 * k + 1]), ov[2 * k]), ov[2 * k + 1]));
+              else
+                d = __fmul_rn(0.25f, __fadd_rn(__fadd_rn(__fadd_rn(prev[2 * k], prev[2 * k + 1]), ov[2 * k]), ov[2 * k + 1]));
+              dec_out[(img * (int64_t)ddh + (y >> 1)) * ddw + xd] = d;
+            }
+          }
+        }
+#pragma unroll
+        for (int cc = 0; cc < VX; ++cc) prev[cc] = ov[cc];
       }
     }
     uses += nchunks;
@@ -596,8 +616,39 @@ __global__ void __launch_bounds__(kBlurWarps * 32) blur5_tma_kernel(const __grid
 
 // Second half of downsample: 5x5 binomial SAME/REPLICATE over already
 // decimated images (dh x dw each, from the fused moments kernel).
+// 2x2 block means of n_images h x w images (the first half of downsample,
+// ttc.py:202-203), for the blur fallbacks that do not emit them.
 template <typename T>
-int launch_blur_dec(const T* dec, int64_t n_images, int h, int w, T* out, cudaStream_t st) {
+__global__ void decimate_kernel(const T* __restrict__ in, int64_t n_images, int h, int w, T* __restrict__ out) {
+  const int dh = h / 2, dw = w / 2;
+  const int64_t n = n_images * dh * dw;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int xd = (int)(i % dw);
+    const int64_t t = i / dw;
+    const int yd = (int)(t % dh);
+    const int64_t img = t / dh;
+    const T* p0 = in + (img * h + 2 * yd) * (int64_t)w + 2 * xd;
+    const T* p1 = p0 + w;
+    if constexpr (sizeof(T) == 8)
+      out[i] = __dmul_rn(0.25, __dadd_rn(__dadd_rn(__dadd_rn(p0[0], p0[1]), p1[0]), p1[1]));
+    else
+      out[i] = __fmul_rn(0.25f, __fadd_rn(__fadd_rn(__fadd_rn(p0[0], p0[1]), p1[0]), p1[1]));
+  }
+}
+
+template <typename T>
+int launch_decimate(const T* in, int64_t n_images, int h, int w, T* out, cudaStream_t st) {
+  const int64_t n = n_images * (h / 2) * (w / 2);
+  if (n == 0) return CT_OK;
+  decimate_kernel<T><<<(unsigned)std::min<int64_t>(cdiv(n, 256), (int64_t)num_sms() * 16), 256, 0, st>>>(
+      in, n_images, h, w, out);
+  return check_launch("decimate");
+}
+
+// blur of the block means `dec` (images of (h/2) x (w/2)) into `out`; with
+// dec_out non-null also the block means of `out` (the next level's `dec`).
+template <typename T>
+int launch_blur_dec(const T* dec, int64_t n_images, int h, int w, T* out, cudaStream_t st, T* dec_out = nullptr) {
   const int dh = h / 2, dw = w / 2;
   if (n_images == 0 || dh == 0 || dw == 0) return CT_OK;
   constexpr int VX = 16 / sizeof(T);
@@ -618,7 +669,7 @@ int launch_blur_dec(const T* dec, int64_t n_images, int h, int w, T* out, cudaSt
       int per_sm = 1;
       CT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlurWarps * 32, smem));
       const int64_t blocks = std::min<int64_t>(cdiv(items, kBlurWarps), (int64_t)num_sms() * std::max(1, per_sm));
-      kern<<<(unsigned)blocks, kBlurWarps * 32, smem, st>>>(tmap, n_images, dh, dw, strip, out);
+      kern<<<(unsigned)blocks, kBlurWarps * 32, smem, st>>>(tmap, n_images, dh, dw, strip, out, dec_out);
       return check_launch("pyramid_blur_tma");
     }
   }
@@ -630,12 +681,16 @@ int launch_blur_dec(const T* dec, int64_t n_images, int h, int w, T* out, cudaSt
     const int64_t items = n_images * cdiv(dh, strip) * cdiv(dw, 32 * VX);
     const int64_t blocks = std::min<int64_t>(cdiv(items, 8), (int64_t)num_sms() * 8 * 4);
     blur5_rows_kernel<T><<<(unsigned)blocks, 256, 0, st>>>(dec, n_images, dh, dw, strip, out);
-    return check_launch("pyramid_blur_rows");
+    int rc = check_launch("pyramid_blur_rows");
+    if (rc || dec_out == nullptr) return rc;
+    return launch_decimate<T>(out, n_images, dh, dw, dec_out, st);
   }
   const int tiles = ((dh + kPyTileY - 1) / kPyTileY) * ((dw + kPyTileX - 1) / kPyTileX);
   dim3 grid((unsigned)tiles, (unsigned)std::min<int64_t>(n_images, 65535));
   pyramid_down_kernel<T, false, false><<<grid, 256, 0, st>>>(dec, n_images, h, w, out);
-  return check_launch("pyramid_blur");
+  int rc = check_launch("pyramid_blur");
+  if (rc || dec_out == nullptr) return rc;
+  return launch_decimate<T>(out, n_images, dh, dw, dec_out, st);
 }
 
 int launch_solve(const double* sums, int64_t count, double c_min, int level, double* est, int64_t stride,
@@ -646,6 +701,8 @@ int launch_solve(const double* sums, int64_t count, double c_min, int level, dou
 }
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+constexpr int kMaxPyr = 32;  // pyramid levels (extents < 2^31 halve at most 31 times)
 
 // number of pyramid levels the reference visits for frames of h x w
 int ms_levels(int h, int w, int max_level) {
@@ -661,25 +718,134 @@ int ms_levels(int h, int w, int max_level) {
   return n;
 }
 
+// Multiscale epilogue, one warp per frame pair: for every level the
+// fixed-order sum of the band partials (the order of moments_finalize_kernel),
+// the solve (solve_one) and then the greedy level walk
+// (multiscale_select_kernel) -- one launch instead of two per level plus one.
+struct EpiLevels {
+  const double* partials[kMaxPyr];
+  int units[kMaxPyr];
+  double count[kMaxPyr];
+};
+
+__global__ void __launch_bounds__(256) ms_epilogue_kernel(const EpiLevels L, int nl, int64_t np, double c_min,
+                                                          double* est) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t pr = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); pr < np; pr += nwarps) {
+    double best[10], cur[10], prev = 0.0;
+    for (int l = 0; l < nl; ++l) {
+      double acc[10];
+#pragma unroll
+      for (int q = 0; q < 10; ++q) acc[q] = 0.0;
+      const int units = L.units[l];
+      for (int u = lane; u < units; u += 32) {
+        const double2* r = reinterpret_cast<const double2*>(L.partials[l] + (pr * units + u) * 10);
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+          const double2 v = r[k];
+          acc[2 * k] += v.x;
+          acc[2 * k + 1] += v.y;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 10; ++q)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+      int stop = 0;
+      if (lane == 0) {  // the greedy walk, one level at a time (stops where the reference stops)
+        double sm[11];
+#pragma unroll
+        for (int q = 0; q < 10; ++q) sm[q] = acc[q];
+        sm[10] = L.count[l];
+        solve_one(sm, c_min, l, cur);
+        const double mf = cur[7];
+        if (l == 0 || mf < best[7])
+#pragma unroll
+          for (int q = 0; q < 10; ++q) best[q] = cur[q];
+        if (l > 0 && !(mf < prev * (1.0 - 1e-3))) stop = 1;
+        prev = mf;
+      }
+      if (__shfl_sync(0xffffffffu, stop, 0)) break;
+    }
+    if (lane == 0)
+#pragma unroll
+      for (int q = 0; q < 10; ++q) est[pr * 10 + q] = best[q];
+  }
+}
+
+// Workspace layout of the multiscale pipeline (run_seq with max_level >= 0 and
+// pyr_moments): levels 1..nl-1 and their block-mean inputs, then one partials
+// buffer per level.
+template <typename T>
+struct PyrPlan {
+  int nl = 0;
+  int lh[kMaxPyr], lw[kMaxPyr];
+  size_t level_off[kMaxPyr], dec_off[kMaxPyr], part_off[kMaxPyr];
+  size_t total = 0;
+  PyrPlan(int64_t nv, int nf, int h, int w, int n_levels) {
+    const int dt = sizeof(T) == 8 ? CT_F64 : CT_F32;
+    nl = n_levels;
+    lh[0] = h;
+    lw[0] = w;
+    for (int l = 1; l < nl; ++l) {
+      lh[l] = lh[l - 1] / 2;
+      lw[l] = lw[l - 1] / 2;
+      const size_t bytes = align256((size_t)nv * nf * lh[l] * lw[l] * sizeof(T));
+      level_off[l] = total;
+      total += bytes;
+      dec_off[l] = total;
+      total += bytes;
+    }
+    for (int l = 0; l < nl; ++l) {
+      part_off[l] = total;
+      total += align256(moments_workspace(dt, nv, nf, lh[l], lw[l]));
+    }
+  }
+};
+
+// Levels 0..nl-1 of the multiscale pyramid and their band partials: level 0's
+// moments also write its 2x2 block means, each blur also writes the next
+// level's block means, and levels 1.. run as one moments launch.
+template <typename T>
+int pyr_partials(const T* frames, int64_t nv, int nf, const PyrPlan<T>& P, char* ws, cudaStream_t st) {
+  const int dt = sizeof(T) == 8 ? CT_F64 : CT_F32;
+  const int nl = P.nl;
+  auto level = [&](int l) { return reinterpret_cast<T*>(ws + P.level_off[l]); };
+  auto dec = [&](int l) { return reinterpret_cast<T*>(ws + P.dec_off[l]); };
+  auto part = [&](int l) { return reinterpret_cast<double*>(ws + P.part_off[l]); };
+  MomentLevel l0{frames, P.lh[0], P.lw[0], part(0), nl > 1 ? (void*)dec(1) : nullptr};
+  int rc = moments_levels_launch(dt, &l0, 1, nv, nf, 1, st);
+  if (rc) return rc;
+  for (int l = 1; l < nl; ++l) {
+    rc = launch_blur_dec<T>(dec(l), nv * nf, P.lh[l - 1], P.lw[l - 1], level(l), st, l + 1 < nl ? dec(l + 1) : nullptr);
+    if (rc) return rc;
+  }
+  MomentLevel lv[kMaxPyr];
+  for (int l = 1; l < nl; ++l) lv[l - 1] = MomentLevel{level(l), P.lh[l], P.lw[l], part(l), nullptr};
+  for (int l = 0; l < nl - 1 && rc == 0; l += kMomentLevelsPerLaunch)
+    rc = moments_levels_launch(dt, lv + l, std::min(kMomentLevelsPerLaunch, nl - 1 - l), nv, nf, 1, st);
+  return rc;
+}
+
 template <typename T>
 size_t run_seq_ws(int64_t nv, int nf, int h, int w, int level, int max_level) {
   const bool ms = max_level >= 0;
-  const int nl = ms ? ms_levels(h, w, max_level) : level + 1;
+  const int64_t np = nv * (nf - 1);
+  if (ms) {
+    const int nl = ms_levels(h, w, max_level);
+    return nl > 0 ? PyrPlan<T>(nv, nf, h, w, nl).total : 0;
+  }
   const int dt = sizeof(T) == 8 ? CT_F64 : CT_F32;
-  size_t total = 0, mom = 0;
+  size_t total = 0;
   int lh = h, lw = w;
-  for (int l = 0; l < std::max(nl, 1); ++l) {
+  for (int l = 0; l <= level; ++l) {
     if (l > 0) total += align256((size_t)nv * nf * lh * lw * sizeof(T));
-    if (ms || l == level) mom = std::max(mom, moments_workspace(dt, nv, nf, lh, lw));
+    if (l == level) total += align256(moments_workspace(dt, nv, nf, lh, lw));
     lh /= 2;
     lw /= 2;
   }
-  if (ms && nl > 1) total += align256((size_t)nv * nf * (h / 2) * (w / 2) * sizeof(T));
-  const int64_t np = nv * (nf - 1);
-  total += align256(mom);
-  total += align256((size_t)np * 11 * sizeof(double));
-  if (ms) total += align256((size_t)np * std::max(nl, 1) * 10 * sizeof(double));
-  return total;
+  return total + align256((size_t)np * 11 * sizeof(double));
 }
 
 template <typename T>
@@ -690,63 +856,46 @@ int run_seq(const T* frames, int64_t nv, int nf, int h, int w, int level, int ma
   if (np <= 0) return CT_OK;
   const size_t need = run_seq_ws<T>(nv, nf, h, w, level, max_level);
   CT_REQUIRE(ws != nullptr && ws_bytes >= need, "run_sequence workspace too small (%zu < %zu)", ws_bytes, need);
-  const int nl = ms ? ms_levels(h, w, max_level) : level + 1;
   const int dt = sizeof(T) == 8 ? CT_F64 : CT_F32;
   char* cur = reinterpret_cast<char*>(ws);
-  const T* level_ptr[32];
-  int level_h[32], level_w[32];
-  level_ptr[0] = frames;
-  level_h[0] = h;
-  level_w[0] = w;
-  T* level_buf[32] = {nullptr};
-  for (int l = 1; l < std::max(nl, 1); ++l) {  // level storage 1..nl-1
-    level_h[l] = level_h[l - 1] / 2;
-    level_w[l] = level_w[l - 1] / 2;
-    level_buf[l] = reinterpret_cast<T*>(cur);
-    level_ptr[l] = level_buf[l];
-    cur += align256((size_t)nv * nf * level_h[l] * level_w[l] * sizeof(T));
-  }
-  // the multiscale path decimates inside the moments kernel (scratch = one level-1 sized buffer)
-  T* dec_scratch = nullptr;
-  if (ms && nl > 1) {
-    dec_scratch = reinterpret_cast<T*>(cur);
-    cur += align256((size_t)nv * nf * level_h[1] * level_w[1] * sizeof(T));
-  }
-  size_t mom = 0;
-  for (int l = 0; l < nl; ++l)
-    if (ms || l == level) mom = std::max(mom, moments_workspace(dt, nv, nf, level_h[l], level_w[l]));
-  void* mom_ws = cur;
-  cur += align256(mom);
-  double* sums = reinterpret_cast<double*>(cur);
-  cur += align256((size_t)np * 11 * sizeof(double));
   if (!ms) {
+    const T* src = frames;
+    int lh = h, lw = w;
     for (int l = 1; l <= level; ++l) {
-      int rc = launch_pyramid<T>(level_ptr[l - 1], nv * nf, level_h[l - 1], level_w[l - 1], level_buf[l], st);
+      T* dst = reinterpret_cast<T*>(cur);
+      cur += align256((size_t)nv * nf * (lh / 2) * (lw / 2) * sizeof(T));
+      int rc = launch_pyramid<T>(src, nv * nf, lh, lw, dst, st);
       if (rc) return rc;
+      src = dst;
+      lh /= 2;
+      lw /= 2;
     }
-    int rc = moments_launch(dt, level_ptr[level], nv, nf, level_h[level], level_w[level], 1, sums, mom_ws, mom, st);
+    const size_t mom = moments_workspace(dt, nv, nf, lh, lw);
+    void* mom_ws = cur;
+    cur += align256(mom);
+    double* sums = reinterpret_cast<double*>(cur);
+    int rc = moments_launch(dt, src, nv, nf, lh, lw, 1, sums, mom_ws, mom, st);
     if (rc) return rc;
     return launch_solve(sums, np, c_min, level, est, 10, st);
   }
+  const int nl = ms_levels(h, w, max_level);
   if (nl == 0) {
     multiscale_select_kernel<<<(unsigned)cdiv(np, 128), 128, 0, st>>>(nullptr, np, 0, est);
     return check_launch("multiscale_select");
   }
-  double* est_levels = reinterpret_cast<double*>(cur);
+  CT_REQUIRE(nl <= kMaxPyr, "too many pyramid levels");
+  const PyrPlan<T> P(nv, nf, h, w, nl);
+  int rc = pyr_partials<T>(frames, nv, nf, P, cur, st);
+  if (rc) return rc;
+  EpiLevels L;
   for (int l = 0; l < nl; ++l) {
-    const bool next = l + 1 < nl;
-    int rc = moments_launch(dt, level_ptr[l], nv, nf, level_h[l], level_w[l], 1, sums, mom_ws, mom, st,
-                            next ? dec_scratch : nullptr);
-    if (rc) return rc;
-    rc = launch_solve(sums, np, c_min, l, est_levels + l * 10, (int64_t)nl * 10, st);
-    if (rc) return rc;
-    if (next) {
-      rc = launch_blur_dec<T>(dec_scratch, nv * nf, level_h[l], level_w[l], level_buf[l + 1], st);
-      if (rc) return rc;
-    }
+    L.partials[l] = reinterpret_cast<const double*>(cur + P.part_off[l]);
+    L.units[l] = moments_units(dt, nv, nf, P.lh[l], P.lw[l]);
+    L.count[l] = (double)(P.lh[l] - 3) * (double)(P.lw[l] - 3);
   }
-  multiscale_select_kernel<<<(unsigned)cdiv(np, 128), 128, 0, st>>>(est_levels, np, nl, est);
-  return check_launch("multiscale_select");
+  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(np, 8), (int64_t)num_sms() * 8));
+  ms_epilogue_kernel<<<blocks, 256, 0, st>>>(L, nl, np, c_min, est);
+  return check_launch("ms_epilogue");
 }
 
 // Per-level normal-system sums of every frame pair on the multiscale pyramid
@@ -756,17 +905,7 @@ int run_seq(const T* frames, int64_t nv, int nf, int h, int w, int level, int ma
 // the 5x5 binomial), exactly the sums run_sequence's multiscale walk solves.
 template <typename T>
 size_t pyr_ws(int64_t nv, int nf, int h, int w, int levels) {
-  const int dt = sizeof(T) == 8 ? CT_F64 : CT_F32;
-  size_t total = 0, mom = 0;
-  int lh = h, lw = w;
-  for (int l = 0; l < levels; ++l) {
-    if (l > 0) total += align256((size_t)nv * nf * lh * lw * sizeof(T));
-    mom = std::max(mom, moments_workspace(dt, nv, nf, lh, lw));
-    lh /= 2;
-    lw /= 2;
-  }
-  if (levels > 1) total += align256((size_t)nv * nf * (h / 2) * (w / 2) * sizeof(T));
-  return total + align256(mom);
+  return PyrPlan<T>(nv, nf, h, w, levels).total;
 }
 
 template <typename T>
@@ -774,40 +913,19 @@ int pyr_moments(const T* frames, int64_t nv, int nf, int h, int w, int levels, d
                 size_t ws_bytes, cudaStream_t st) {
   const int64_t np = nv * (nf - 1);
   if (np <= 0) return CT_OK;
+  CT_REQUIRE(levels <= kMaxPyr, "too many pyramid levels");
   const size_t need = pyr_ws<T>(nv, nf, h, w, levels);
   CT_REQUIRE(ws != nullptr && ws_bytes >= need, "pyramid_moments workspace too small (%zu < %zu)", ws_bytes, need);
   const int dt = sizeof(T) == 8 ? CT_F64 : CT_F32;
   char* cur = reinterpret_cast<char*>(ws);
-  const T* level_ptr[32];
-  T* level_buf[32] = {nullptr};
-  int level_h[32], level_w[32];
-  level_ptr[0] = frames;
-  level_h[0] = h;
-  level_w[0] = w;
-  for (int l = 1; l < levels; ++l) {
-    level_h[l] = level_h[l - 1] / 2;
-    level_w[l] = level_w[l - 1] / 2;
-    level_buf[l] = reinterpret_cast<T*>(cur);
-    level_ptr[l] = level_buf[l];
-    cur += align256((size_t)nv * nf * level_h[l] * level_w[l] * sizeof(T));
-  }
-  T* dec_scratch = nullptr;
-  if (levels > 1) {
-    dec_scratch = reinterpret_cast<T*>(cur);
-    cur += align256((size_t)nv * nf * level_h[1] * level_w[1] * sizeof(T));
-  }
-  size_t mom = 0;
-  for (int l = 0; l < levels; ++l) mom = std::max(mom, moments_workspace(dt, nv, nf, level_h[l], level_w[l]));
-  void* mom_ws = cur;
+  const PyrPlan<T> P(nv, nf, h, w, levels);
+  int rc = pyr_partials<T>(frames, nv, nf, P, cur, st);
+  if (rc) return rc;
   for (int l = 0; l < levels; ++l) {
-    const bool next = l + 1 < levels;
-    int rc = moments_launch(dt, level_ptr[l], nv, nf, level_h[l], level_w[l], 1, sums + (size_t)l * np * 11, mom_ws,
-                            mom, st, next ? dec_scratch : nullptr);
+    const double count = (double)(P.lh[l] - 3) * (double)(P.lw[l] - 3);
+    rc = partials_finalize(reinterpret_cast<const double*>(cur + P.part_off[l]), np,
+                           moments_units(dt, nv, nf, P.lh[l], P.lw[l]), count, sums + (size_t)l * np * 11, st);
     if (rc) return rc;
-    if (next) {
-      rc = launch_blur_dec<T>(dec_scratch, nv * nf, level_h[l], level_w[l], level_buf[l + 1], st);
-      if (rc) return rc;
-    }
   }
   return CT_OK;
 }
