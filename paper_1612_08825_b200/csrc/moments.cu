@@ -87,6 +87,29 @@ __device__ __forceinline__ void write_dec(const MomentArgs& a, const T* buf, int
   const int dy0 = gy0 >> 1, dx0 = cx0 >> 1;
   const int ndy = min(BR / 2, a.dh - dy0);
   const int ndx = min((a.tile_cols + 1) >> 1, a.dw - dx0);
+  if constexpr (sizeof(T) == 4) {
+    if ((a.dw & 1) == 0) {  // two dec columns per thread: one 16-byte smem read per source row, 8-byte stores
+      constexpr int DC2 = DC / 2;
+      static_assert(NT % DC2 == 0, "write_dec maps DC/2 dec column pairs per thread row");
+      const int xp = tid % DC2;  // dec columns 2xp, 2xp + 1
+      if (ndy <= 0 || 2 * xp >= ndx) return;
+      const bool two = 2 * xp + 1 < ndx;
+      float* dst = reinterpret_cast<float*>(a.dec) + ((v * a.n_frames + f) * (int64_t)a.dh + dy0) * a.dw + dx0 + 2 * xp;
+#pragma unroll 4
+      for (int yy = tid / DC2; yy < ndy; yy += NT / DC2) {
+        const float4 q0 = *reinterpret_cast<const float4*>(buf + (2 * yy) * BC + 4 * xp);
+        const float4 q1 = *reinterpret_cast<const float4*>(buf + (2 * yy + 1) * BC + 4 * xp);
+        const float d0 = __fmul_rn(0.25f, __fadd_rn(__fadd_rn(__fadd_rn(q0.x, q0.y), q1.x), q1.y));
+        const float d1 = __fmul_rn(0.25f, __fadd_rn(__fadd_rn(__fadd_rn(q0.z, q0.w), q1.z), q1.w));
+        float* o = dst + (int64_t)yy * a.dw;
+        if (two)
+          *reinterpret_cast<float2*>(o) = make_float2(d0, d1);
+        else
+          o[0] = d0;
+      }
+      return;
+    }
+  }
   const int xx = tid % DC;  // dec column of this thread
   if (ndy <= 0 || xx >= ndx) return;
   T* dst = reinterpret_cast<T*>(a.dec) + ((v * a.n_frames + f) * (int64_t)a.dh + dy0) * a.dw + dx0 + xx;

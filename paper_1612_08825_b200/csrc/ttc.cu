@@ -718,28 +718,30 @@ int ms_levels(int h, int w, int max_level) {
   return n;
 }
 
-// Multiscale epilogue, one warp per frame pair: for every level the
-// fixed-order sum of the band partials (the order of moments_finalize_kernel),
-// the solve (solve_one) and then the greedy level walk
-// (multiscale_select_kernel) -- one launch instead of two per level plus one.
+// Multiscale epilogue, one CTA of kEpiThreads per frame pair: for every level
+// a fixed-order sum of the band partials (thread t adds units t, t + 128, ...,
+// then a warp butterfly and the four warp sums in order), the levels' solves
+// side by side on the lanes of warp 0 (solve_one), and then the greedy level
+// walk of multiscale_select_kernel -- one launch instead of two per level plus one.
 struct EpiLevels {
   const double* partials[kMaxPyr];
   int units[kMaxPyr];
   double count[kMaxPyr];
 };
+constexpr int kEpiThreads = 128;
 
-__global__ void __launch_bounds__(256) ms_epilogue_kernel(const EpiLevels L, int nl, int64_t np, double c_min,
-                                                          double* est) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t pr = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); pr < np; pr += nwarps) {
-    double best[10], cur[10], prev = 0.0;
+__global__ void __launch_bounds__(kEpiThreads) ms_epilogue_kernel(const EpiLevels L, int nl, int64_t np,
+                                                                  double c_min, double* est) {
+  constexpr int NW = kEpiThreads / 32;
+  __shared__ double red[kMaxPyr][NW][10];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (int64_t pr = blockIdx.x; pr < np; pr += gridDim.x) {
     for (int l = 0; l < nl; ++l) {
       double acc[10];
 #pragma unroll
       for (int q = 0; q < 10; ++q) acc[q] = 0.0;
       const int units = L.units[l];
-      for (int u = lane; u < units; u += 32) {
+      for (int u = tid; u < units; u += kEpiThreads) {
         const double2* r = reinterpret_cast<const double2*>(L.partials[l] + (pr * units + u) * 10);
 #pragma unroll
         for (int k = 0; k < 5; ++k) {
@@ -752,25 +754,48 @@ __global__ void __launch_bounds__(256) ms_epilogue_kernel(const EpiLevels L, int
       for (int q = 0; q < 10; ++q)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
-      int stop = 0;
-      if (lane == 0) {  // the greedy walk, one level at a time (stops where the reference stops)
+      if (lane < 10) {
+        double mineq = acc[0];
+#pragma unroll
+        for (int q = 1; q < 10; ++q)
+          if (lane == q) mineq = acc[q];
+        red[l][wid][lane] = mineq;
+      }
+    }
+    __syncthreads();
+    if (wid == 0) {
+      double e[10];
+      if (lane < nl) {  // the levels' solves run side by side
         double sm[11];
 #pragma unroll
-        for (int q = 0; q < 10; ++q) sm[q] = acc[q];
-        sm[10] = L.count[l];
-        solve_one(sm, c_min, l, cur);
-        const double mf = cur[7];
-        if (l == 0 || mf < best[7])
+        for (int q = 0; q < 10; ++q) {
+          double t = 0.0;
 #pragma unroll
-          for (int q = 0; q < 10; ++q) best[q] = cur[q];
-        if (l > 0 && !(mf < prev * (1.0 - 1e-3))) stop = 1;
+          for (int w = 0; w < NW; ++w) t += red[lane][w][q];
+          sm[q] = t;
+        }
+        sm[10] = L.count[lane];
+        solve_one(sm, c_min, lane, e);
+      }
+      // the greedy walk over the levels (multiscale_select_kernel's loop)
+      int b = 0;
+      double prev = 0.0, bmf = __shfl_sync(0xffffffffu, e[7], 0);
+      for (int l = 0; l < nl; ++l) {
+        const double mf = __shfl_sync(0xffffffffu, e[7], l);
+        if (l > 0 && mf < bmf) {
+          b = l;
+          bmf = mf;
+        }
+        if (l > 0 && !(mf < prev * (1.0 - 1e-3))) break;
         prev = mf;
       }
-      if (__shfl_sync(0xffffffffu, stop, 0)) break;
-    }
-    if (lane == 0)
 #pragma unroll
-      for (int q = 0; q < 10; ++q) est[pr * 10 + q] = best[q];
+      for (int q = 0; q < 10; ++q) {
+        const double val = __shfl_sync(0xffffffffu, e[q], b);
+        if (lane == 0) est[pr * 10 + q] = val;
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -893,8 +918,8 @@ int run_seq(const T* frames, int64_t nv, int nf, int h, int w, int level, int ma
     L.units[l] = moments_units(dt, nv, nf, P.lh[l], P.lw[l]);
     L.count[l] = (double)(P.lh[l] - 3) * (double)(P.lw[l] - 3);
   }
-  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(np, 8), (int64_t)num_sms() * 8));
-  ms_epilogue_kernel<<<blocks, 256, 0, st>>>(L, nl, np, c_min, est);
+  const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>(np, (int64_t)num_sms() * 16));
+  ms_epilogue_kernel<<<blocks, kEpiThreads, 0, st>>>(L, nl, np, c_min, est);
   return check_launch("ms_epilogue");
 }
 
