@@ -216,7 +216,7 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
-DP_PER_PX = 20 + 7 / 16
+DP_PER_PX = 722.086e6 * 32 / (256 * 63 * 255 * 255)  # ncu FP64 warp instructions x 32 lanes per grid pixel (22.0)
 FP64_LANE_PEAK = 32.2e12 / 2
 
 
@@ -304,7 +304,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--videos", type=int, default=256, help="cfg2 videos per GPU per step")
-    ap.add_argument("--ref-videos", type=int, default=2, help="videos per step for --impl reference")
+    ap.add_argument("--ref-videos", type=int, default=16, help="videos per step for --impl reference (enough pairs for every host thread)")
     ap.add_argument("--e2e-videos", type=int, default=32)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-secondary", action="store_true")
@@ -377,17 +377,18 @@ def main():
     # roofline of the dominant kernel: its CUDA-event time inside the timed region (t_k above)
     hbm, peak_kind = load_peaks()
     achieved = V * (NFRAMES - 1) * BYTES_PER_EST / t_k / 1e9
-    tr = load_ncu_traffic("ttc_moments_kernel<double>/cfg2")
+    tr = load_ncu_traffic("ttc_moments_ws_kernel<double>/cfg2")
     traffic = None
     if tr and tr.get("videos"):
         traffic = tr["bytes_per_launch"] * V / tr["videos"]  # scaled to this launch's video count
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
             "traffic": traffic, "traffic_unit": "bytes/launch (dram read+write, ncu --set full, profiles/)",
-            "algorithmic_bytes_per_launch": V * (NFRAMES - 1) * BYTES_PER_EST, "kernel": "ttc_moments_kernel<double> (+ finalize)", "peak_kind": peak_kind,
+            "algorithmic_bytes_per_launch": V * (NFRAMES - 1) * BYTES_PER_EST, "kernel": "ttc_moments_ws_kernel<double> (+ finalize)", "peak_kind": peak_kind,
             "kernel_ms": t_k * 1e3, "step_ms": dt / args.steps * 1e3,
             "kernel_timing": "CUDA events around ct_ttc_moments in every timed step, on its stream, max over ranks",
-            # the kernel is FP64-issue bound (profiles/r01_moments_probe.md): 20 FP64
-            # instructions per grid pixel + 7 per band-halo row (16-row bands)
+            # the kernel is FP64-issue bound (profiles/r01_ttc_moments_ws_f64_cfg2.txt):
+            # 722.1 M FP64 warp instructions per 256-video launch = 21.86 per thread-pixel
+            # (sweep 20 + 7/16 band-halo row + the per-pair epilogue and warp reduction)
             "fp64_pipe": {"dp_instr_per_grid_px": DP_PER_PX,
                           "achieved_lane_ops_per_s": DP_PER_PX * V * (NFRAMES - 1) * 255 * 255 / t_k,
                           "peak_lane_ops_per_s": FP64_LANE_PEAK,
