@@ -487,9 +487,9 @@ struct SmemWS {  // warp-streaming kernel: NB frame-band buffers + per-buffer / 
 //     so fp32 bands run 256 threads (16 warps per SM) with two columns per
 //     thread.
 #ifndef CT_MOM_MINB32
-#define CT_MOM_MINB32 0
+#define CT_MOM_MINB32 3
 #endif
-// resident CTAs per SM the register budget is sized for (fp32 probing: CT_MOM_MINB32)
+// resident CTAs per SM the register budget is sized for (fp32: CT_MOM_MINB32, see band_rows)
 template <typename T, int BC, int RS>
 constexpr int ws_min_blocks() {
   return (sizeof(T) == 4 && CT_MOM_MINB32 > 0) ? CT_MOM_MINB32 : ((512 / BC) / RS > 0 ? (512 / BC) / RS : 1);
@@ -865,15 +865,13 @@ inline unsigned finalize_grid(int64_t n_sys) {
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(n_sys, kFinWarps), (int64_t)num_sms() * 8));
 }
 
-// Band height: 16 rows for f64 (3 x 35 KB buffers, 2 CTAs/SM, FP64-bound),
-// 32 rows for f32 (3 x 34 KB; the cheaper FP32 math needs bigger TMA
-// transfers and fewer per-pair reductions per pixel).
-// Band height: 16 rows for f64 (3 x 35 KB buffers, 2 CTAs/SM, FP64-bound),
-// 32 rows for f32 (3 x 34 KB): per-pair reduction overhead is amortised over
-// more pixels, which matters for the cheaper FP32 math (measured: 16 rows with
-// a 6-deep ring is 25% slower than 32 rows with 3 buffers).
+// Band height: 16 rows for f64 (3 x 35 KB buffers, 2 CTAs/SM, FP64-bound);
+// 20 rows for f32 (3 x 21 KB, 3 CTAs/SM of 4 warps with <= 170 registers):
+// the fp32 kernel is latency-bound, and 20-row bands at 12 warps/SM beat
+// 32-row bands at 8 warps/SM (1080p 0.552 -> 0.537 ms) as well as 14-22 rows
+// and 4-deep rings (profiles/r01_moments_probe.md).
 #ifndef CT_MOM_BR32
-#define CT_MOM_BR32 32
+#define CT_MOM_BR32 20
 #endif
 #ifndef CT_MOM_NB32
 #define CT_MOM_NB32 3
