@@ -486,13 +486,18 @@ struct SmemWS {  // warp-streaming kernel: NB frame-band buffers + per-buffer / 
 //     column groups (CPT columns each) and the RS groups split the band rows,
 //     so fp32 bands run 256 threads (16 warps per SM) with two columns per
 //     thread.
+#ifndef CT_MOM_MINB64
+#define CT_MOM_MINB64 0
+#endif
 #ifndef CT_MOM_MINB32
 #define CT_MOM_MINB32 3
 #endif
 // resident CTAs per SM the register budget is sized for (fp32: CT_MOM_MINB32, see band_rows)
 template <typename T, int BC, int RS>
 constexpr int ws_min_blocks() {
-  return (sizeof(T) == 4 && CT_MOM_MINB32 > 0) ? CT_MOM_MINB32 : ((512 / BC) / RS > 0 ? (512 / BC) / RS : 1);
+  return (sizeof(T) == 4 && CT_MOM_MINB32 > 0)   ? CT_MOM_MINB32
+         : (sizeof(T) == 8 && CT_MOM_MINB64 > 0) ? CT_MOM_MINB64
+                                                 : ((512 / BC) / RS > 0 ? (512 / BC) / RS : 1);
 }
 
 template <typename T, int BR, int NB, int BC, int CPT, int RS>
