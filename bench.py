@@ -293,6 +293,13 @@ def secondary_configs(quick: bool):
                                          "roofline": {"bound": "hbm", "achieved": bytes_ / t / 1e9, "peak": hbm,
                                                       "unit": "GB/s", "frac": bytes_ / t / 1e9 / hbm,
                                                       "note": "whole pipeline (pyramid + 4 moment levels + solve)"}}
+    # the fused fp32 moments kernel alone on the same frames: the level-0 run_sequence pass
+    t0 = timeit(lambda: ct.run_sequence_batch(fr, level=0), 3)
+    out["cfg5_multiscale_fp32_1080p"]["level0_fused_kernel"] = {
+        "ms_per_step": t0 * 1e3, "est_s": n_est / t0,
+        "roofline": {"bound": "hbm", "achieved": bytes_ / t0 / 1e9, "peak": hbm, "unit": "GB/s",
+                     "frac": bytes_ / t0 / 1e9 / hbm,
+                     "note": "ttc_moments_ws_kernel<float> + finalize + solve over the level-0 frames"}}
     del fr
     return out
 
