@@ -486,7 +486,18 @@ __global__ void __launch_bounds__(256) blur5_rows_kernel(const T* __restrict__ i
 // memory.  REPLICATE clamping: rows outside the image reuse the nearest
 // image row's horizontal sums, columns outside take the edge value.  Same
 // FMA chains as blur5_rows_kernel (bit-identical).
-constexpr int kBlurRch = 4, kBlurStages = 4, kBlurWarps = 8;
+// ring of 3 stages x 8 rows per warp, 4 warps per CTA: cfg5 levels 1-3 blur
+// 171 -> 160 us per 128-frame video against 4 x 4 rows / 8 warps (profiles/r01_moments_probe.md)
+#ifndef CT_BLUR_RCH
+#define CT_BLUR_RCH 8
+#endif
+#ifndef CT_BLUR_STAGES
+#define CT_BLUR_STAGES 3
+#endif
+#ifndef CT_BLUR_WARPS
+#define CT_BLUR_WARPS 4
+#endif
+constexpr int kBlurRch = CT_BLUR_RCH, kBlurStages = CT_BLUR_STAGES, kBlurWarps = CT_BLUR_WARPS;
 
 template <typename T>
 __global__ void __launch_bounds__(kBlurWarps * 32) blur5_tma_kernel(const __grid_constant__ CUtensorMap tmap,
