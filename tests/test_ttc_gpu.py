@@ -335,3 +335,34 @@ def test_pyramid_moments_vs_oracle(dtype):
         lv = [O.downsample(x) for x in lv]
     with pytest.raises(ValueError, match="halvings"):
         ct.pyramid_moments(dev, 7)
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_fused_multiscale_epilogue_matches_composed_stages(dtype):
+    """run_sequence's multiscale pipeline (block means fused into the level-0
+    moments, blurs emitting the next level's block means, levels >= 1 in one
+    moments launch, one finalize + solve + level-walk epilogue) equals the
+    composed C-ABI stages: ct_ttc_pyramid_moments, ct_ttc_solve per level,
+    ct_ttc_multiscale_select.  Same sums up to the reduction order: selected
+    level and degeneracy identical, a/b/c/FOE/TTC within 1e-12 (fp64) or
+    1e-6 (fp32), on a batch of three videos with 1080p-like aspect."""
+    from paper_1612_08825_b200 import _lib
+    L = _lib.load()
+    vids = np.stack([O.generate(384, 216, 7, float(t0), (0.45, 0.55), 40 + v, 0.001)
+                     for v, t0 in enumerate((60.0, 150.0, 400.0))])
+    dev = torch.from_numpy(vids).to(dtype).cuda()
+    nl = 4
+    got = ct.run_sequence_batch(dev, max_level=nl - 1).cpu().numpy()
+    sums = ct.pyramid_moments(dev, nl)                      # [nl, V, n-1, 11]
+    V, npair = sums.shape[1], sums.shape[2]
+    count = V * npair
+    est_levels = torch.empty((count, nl, 10), dtype=torch.float64, device="cuda")
+    for lv in range(nl):
+        e = torch.empty((count, 10), dtype=torch.float64, device="cuda")
+        s = sums[lv].reshape(count, 11).contiguous()
+        _lib.check(L.ct_ttc_solve(_lib.ptr(s), count, 1e-9, lv, _lib.ptr(e), _lib.stream_ptr()))
+        est_levels[:, lv] = e
+    best = torch.empty((count, 10), dtype=torch.float64, device="cuda")
+    _lib.check(L.ct_ttc_multiscale_select(_lib.ptr(est_levels), count, nl, _lib.ptr(best), _lib.stream_ptr()))
+    ref = best.cpu().numpy().reshape(V, npair, 10)
+    assert_est_close(got, ref, 1e-12 if dtype == torch.float64 else 1e-6)
