@@ -4,7 +4,8 @@
 // run_sequence loop ttc.py:299-304).
 //
 // Layout and schedule
-//   * A CTA (256 threads, one grid column each) owns a band of BR grid rows x
+//   * A CTA (256 threads, one grid column each; fp32: 128 threads, two
+//     columns each) owns a band of BR grid rows x
 //     up to 255 grid columns of one video and walks a chunk of consecutive
 //     frames.  Frame bands (BR+1 rows x 256 columns) arrive by TMA into a
 //     ring of NB shared-memory buffers tracked by mbarriers: while pair
@@ -22,9 +23,13 @@
 //     sum(Ey G) = xc S2 + U2, sum(G Et) = xc S4 + U3, sum(G^2) = xc^2 S1 +
 //     2 xc U1 + U4, with the U sums accumulated under band-relative y
 //     weights (see sweep()); ~20 FP64 ops per grid pixel.
-//   * Per pair the 256 per-thread sums are reduced through shared memory in
-//     a fixed tree (the dead previous-frame buffer is the scratch), giving one
-//     partial per band; moments_finalize adds the band partials in a fixed
+//   * Per pair the 256 per-thread sums become one partial per band: in the
+//     warp-streaming kernel (ttc_moments_ws_kernel, used whenever the frames
+//     admit a TMA map) each warp reduces its lanes with a transpose-reduce
+//     butterfly and the last warp to deposit adds the warp partials in warp
+//     order, with no CTA barrier; the CTA-barrier kernel (ttc_moments_kernel,
+//     LDG loader for frames without a TMA map) reduces through shared memory
+//     in a fixed tree.  moments_finalize adds the band partials in a fixed
 //     order.  Results are bit-reproducible and independent of how pairs are
 //     chunked or sharded.
 #include <stdlib.h>
