@@ -443,7 +443,7 @@ def main():
             "config": {"workload": "cfg2 single-scale TTC fp64: 64-frame 256x256 approach videos (t0=100, FOE centre)",
                        "videos_per_gpu_per_step": V, "estimates_per_step": world * V * (NFRAMES - 1),
                        "input_bytes_per_gpu": V * NFRAMES * H * W * 8,
-                       "l2": "inputs larger than L2 (>= 8.6 GB per GPU vs 126 MB)",
+                       "l2": f"inputs larger than L2 ({V * NFRAMES * H * W * 8 / 1e9:.1f} GB per GPU vs 126 MB)",
                        "parallelism": f"dp{world} (independent videos per rank)"},
             "roofline": roof,
             "e2e": e2e,
