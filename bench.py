@@ -281,29 +281,61 @@ def secondary_configs(quick: bool):
     s1, o1 = s4[:1].contiguous(), o4[:1].contiguous()
     out["cfg4_conv2d_fp32_31x31"]["single_call_ms"] = timeit(lambda: ct.direct_batch(s1, k4, out=o1), 10) * 1e3
     del s4, o4, s1, o1
-    # cfg5: multiscale fp32 1080x1920, max_level=3: the full BASELINE stream, 8 videos x 1024 frames
-    # (67.9 GB of frames resident in HBM, all 8 videos in one run_sequence call; quick mode: 1 x 64)
-    nv, nf = (1, 64) if quick else (8, 1024)
-    fr = torch.empty((nv, nf, 1080, 1920), dtype=torch.float32, device="cuda")
-    for v in range(nv):
-        ct.approach_stream(nf, 1080, 1920, seed=1000 + v, dtype=torch.float32, out=fr[v])
-    t = timeit(lambda: ct.run_sequence_batch(fr, max_level=3), 3)
-    n_est = nv * (nf - 1)
-    bytes_ = n_est * 4 * 1080 * 1920
-    out["cfg5_multiscale_fp32_1080p"] = {"est_s": n_est / t, "videos": nv, "frames": nf, "ms_per_step": t * 1e3,
-                                         "input_bytes": nv * nf * 1080 * 1920 * 4,
-                                         "roofline": {"bound": "hbm", "achieved": bytes_ / t / 1e9, "peak": hbm,
-                                                      "unit": "GB/s", "frac": bytes_ / t / 1e9 / hbm,
-                                                      "note": "whole pipeline (pyramid + 4 moment levels + solve)"}}
-    # the fused fp32 moments kernel alone on the same frames: the level-0 run_sequence pass
-    t0 = timeit(lambda: ct.run_sequence_batch(fr, level=0), 3)
-    out["cfg5_multiscale_fp32_1080p"]["level0_fused_kernel"] = {
-        "ms_per_step": t0 * 1e3, "est_s": n_est / t0,
-        "roofline": {"bound": "hbm", "achieved": bytes_ / t0 / 1e9, "peak": hbm, "unit": "GB/s",
-                     "frac": bytes_ / t0 / 1e9 / hbm,
-                     "note": "ttc_moments_ws_kernel<float> + finalize + solve over the level-0 frames"}}
-    del fr
     return out
+
+
+def cfg5_sharded(quick: bool, world: int, rank: int):
+    """BASELINE config 5, the full multiscale stream (8 videos x 1024 frames of 1080x1920 fp32,
+    max_level=3), sharded over the ranks: rank r builds and processes videos [8r/N, 8(r+1)/N) on
+    its own GPU (no data exchange; 8.5 GB of frames per video stay resident).  Timed with CUDA
+    events between barriers, max over ranks; est/s = every pair of every video / that time
+    (strong scaling: the 8-video job is fixed).  quick: 1 video x 64 frames."""
+    import torch
+    import paper_1612_08825_b200 as ct
+    nv_total, nf = (1, 64) if quick else (8, 1024)
+    lo, hi = rank * nv_total // world, (rank + 1) * nv_total // world
+    nv = hi - lo
+    fr = None
+    if nv:
+        fr = torch.empty((nv, nf, 1080, 1920), dtype=torch.float32, device="cuda")
+        for i, v in enumerate(range(lo, hi)):
+            ct.approach_stream(nf, 1080, 1920, seed=1000 + v, dtype=torch.float32, out=fr[i])
+    st = torch.cuda.current_stream()
+
+    def timed(**kw):
+        if nv:
+            ct.run_sequence_batch(fr, **kw)  # warm (workspace allocation)
+        torch.cuda.synchronize()
+        barrier(world)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 3
+        e0.record(st)
+        for _ in range(reps):
+            if nv:
+                ct.run_sequence_batch(fr, **kw)
+        e1.record(st)
+        e1.synchronize()
+        return max_over_ranks(e0.elapsed_time(e1) / reps * 1e-3, world)
+
+    hbm, _ = load_peaks()
+    n_est = nv_total * (nf - 1)
+    bytes_ = n_est * 4 * 1080 * 1920
+    t = timed(max_level=3)
+    t0 = timed(level=0)
+    del fr
+    torch.cuda.empty_cache()
+    return {"est_s": n_est / t, "videos": nv_total, "frames": nf, "n_gpus": world,
+            "videos_per_gpu": f"{nv_total // world}-{-(-nv_total // world)}", "ms_per_step": t * 1e3,
+            "input_bytes": nv_total * nf * 1080 * 1920 * 4,
+            "scaling": "strong (the 8-video job split over the ranks, no data exchange)",
+            "roofline": {"bound": "hbm", "achieved": bytes_ / t / 1e9 / world, "peak": hbm, "unit": "GB/s per GPU",
+                         "frac": bytes_ / t / 1e9 / world / hbm,
+                         "note": "whole pipeline (level-0 moments + block means, blurs, levels 1-3, epilogue)"},
+            "level0_fused_kernel": {
+                "ms_per_step": t0 * 1e3, "est_s": n_est / t0,
+                "roofline": {"bound": "hbm", "achieved": bytes_ / t0 / 1e9 / world, "peak": hbm,
+                             "unit": "GB/s per GPU", "frac": bytes_ / t0 / 1e9 / world / hbm,
+                             "note": "ttc_moments_ws_kernel<float> + finalize + solve over the level-0 frames"}}}
 
 
 def main():
@@ -427,11 +459,19 @@ def main():
     del host
 
     secondary = None
-    if rank == 0 and not args.no_secondary:
+    if not args.no_secondary:
+        if rank == 0:
+            try:
+                secondary = secondary_configs(args.quick)
+            except Exception as exc:  # reported, never silently dropped
+                secondary = {"error": repr(exc)}
+        # config 5 runs on every rank (its videos shard over the GPUs)
         try:
-            secondary = secondary_configs(args.quick)
-        except Exception as exc:  # reported, never silently dropped
-            secondary = {"error": repr(exc)}
+            c5 = cfg5_sharded(args.quick, world, rank)
+        except Exception as exc:
+            c5 = {"error": repr(exc)}
+        if rank == 0:
+            secondary["cfg5_multiscale_fp32_1080p"] = c5
     cpu = cpu_baseline_sample(args.cpu_seconds) if (rank == 0 and world == 1) else None
     if cpu is not None:  # the reference is serial by design; report one core too
         one = cpu_baseline_sample(min(3.0, args.cpu_seconds), threads=1)
