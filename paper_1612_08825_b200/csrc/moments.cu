@@ -901,6 +901,9 @@ constexpr int ring_buffers() {
   return sizeof(T) == 8 ? CT_MOM_NB64 : CT_MOM_NB32;
 }
 
+#ifndef CT_MOM_WAVES
+#define CT_MOM_WAVES 8
+#endif
 #ifndef CT_MOM_MIN_CHUNK
 #define CT_MOM_MIN_CHUNK 4
 #endif
@@ -932,7 +935,7 @@ Plan make_plan(int64_t n_videos, int n_frames, int h, int w) {
   const int n_pairs = n_frames - 1;
   // ~4 waves of resident CTAs (2 per SM), but >= kMinChunk pairs per CTA so the
   // one-frame time halo of each chunk stays small
-  const int64_t target = (int64_t)num_sms() * (512 / BC) * 4;
+  const int64_t target = (int64_t)num_sms() * CT_MOM_WAVES * ws_min_blocks<T, BC, 1>();  // resident CTAs x waves
   const int64_t per_chunk = std::max<int64_t>(1, (int64_t)p.units * n_videos);
   int64_t chunks = std::max<int64_t>(1, (target + per_chunk - 1) / per_chunk);
   chunks = std::min<int64_t>(chunks, std::max(1, n_pairs / kMinChunk));
