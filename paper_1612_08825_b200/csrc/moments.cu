@@ -378,6 +378,74 @@ __device__ __forceinline__ void sweep_c2(const float* __restrict__ A, const floa
   }
 }
 
+// fp64 two-column sweep (CT_MOM_TWO_COL_F64): a thread owns grid columns
+// col, col+1; per frame row one 16-byte load gives (F[col], F[col+1]) and an
+// 8-byte load F[col+2], and the middle column's time sum/difference is shared
+// (19 FP64 operations per grid pixel instead of 20).  Each column keeps
+// sweep()'s per-lane operation order and hands back sweep<RAW>'s raw running
+// sums, so thread_sums<RAW> folds it exactly like the one-column path.  With
+// twice the pixels per lane, the per-pair warp reduction costs half as much
+// per pixel.
+template <int BR, bool CHECK, int BC>
+__device__ __forceinline__ void sweep_c2d(const double* __restrict__ A, const double* __restrict__ B, int col,
+                                          int r_beg, int r_end, double (&m)[2][10]) {
+  double s1[2] = {0, 0}, s2[2] = {0, 0}, s3[2] = {0, 0}, s4[2] = {0, 0}, s5[2] = {0, 0}, s6[2] = {0, 0};
+  double q2[2] = {0, 0}, q3[2] = {0, 0}, q5[2] = {0, 0}, qq3[2] = {0, 0};
+  double hP[2], dP[2], sD[2];
+  auto row = [&](int r, double (&nhP)[2], double (&ndP)[2], double (&nsD)[2]) {
+    const double2 a01 = *reinterpret_cast<const double2*>(A + r * BC + col);
+    const double2 b01 = *reinterpret_cast<const double2*>(B + r * BC + col);
+    const double a2 = A[r * BC + col + 2], b2 = B[r * BC + col + 2];
+    const double P0 = a01.x + b01.x, P1 = a01.y + b01.y, P2 = a2 + b2;
+    const double D0 = b01.x - a01.x, D1 = b01.y - a01.y, D2 = b2 - a2;
+    nhP[0] = P0 + P1;
+    ndP[0] = P1 - P0;
+    nsD[0] = D0 + D1;
+    nhP[1] = P1 + P2;
+    ndP[1] = P2 - P1;
+    nsD[1] = D1 + D2;
+  };
+  row(0, hP, dP, sD);
+#pragma unroll
+  for (int r = 1; r <= BR; ++r) {
+    double nhP[2], ndP[2], nsD[2];
+    row(r, nhP, ndP, nsD);
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      if (!CHECK || (r >= r_beg && r <= r_end)) {
+        const double ex = dP[c] + ndP[c];
+        const double ey = nhP[c] - hP[c];
+        const double et = sD[c] + nsD[c];
+        s1[c] = fma(ex, ex, s1[c]);
+        s2[c] = fma(ex, ey, s2[c]);
+        s3[c] = fma(ey, ey, s3[c]);
+        s4[c] = fma(ex, et, s4[c]);
+        s5[c] = fma(ey, et, s5[c]);
+        s6[c] = fma(et, et, s6[c]);
+      }
+      if (r == 1) {
+        q2[c] = s2[c];
+        q3[c] = s3[c];
+        q5[c] = s5[c];
+        qq3[c] = s3[c];
+      } else {
+        q2[c] += s2[c];
+        q3[c] += s3[c];
+        q5[c] += s5[c];
+        qq3[c] += q3[c];
+      }
+      hP[c] = nhP[c];
+      dP[c] = ndP[c];
+      sD[c] = nsD[c];
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    m[c][0] = s1[c]; m[c][1] = s2[c]; m[c][2] = s3[c]; m[c][3] = s4[c]; m[c][4] = s5[c]; m[c][5] = s6[c];
+    m[c][6] = q2[c]; m[c][7] = q3[c]; m[c][8] = q5[c]; m[c][9] = qq3[c];
+  }
+}
+
 // This thread's ten normal-system sums for one pair (order m00 m01 m02 m11
 // m12 m22 r0 r1 r2 et2, rhs not yet negated) from its per-column sweep
 // sums: the band-relative y weights are shifted by the absolute centred y
@@ -514,10 +582,9 @@ __device__ __forceinline__ void moments_ws_body(const MomentArgs& a, const CUten
   constexpr int NW = S::NW;
   constexpr int HR = BR / RS;        // band rows per row group
   constexpr int LG = 32 / RS;        // lanes per row group
-  static_assert(CPT == 1 || sizeof(T) == 4, "two columns per thread is the fp32 path");
   static_assert(BR % RS == 0 && 32 % RS == 0, "row split");
-  // fp64 single-column sweeps hand back raw running sums (folded in thread_sums)
-  constexpr bool kRaw = sizeof(T) == 8 && CPT == 1;
+  // fp64 sweeps hand back raw running sums (folded in thread_sums)
+  constexpr bool kRaw = sizeof(T) == 8;
   auto buf = [&](int k) { return reinterpret_cast<T*>(smem + (size_t)k * S::buf_bytes); };
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::bars_off);
   int* rel = reinterpret_cast<int*>(smem + S::rel_off);
@@ -582,7 +649,14 @@ __device__ __forceinline__ void moments_ws_body(const MomentArgs& a, const CUten
     const T* Ar = A + r0 * BC;
     const T* Br = B + r0 * BC;
     ACC mc[CPT][10];
-    if constexpr (CPT == 2) {
+    if constexpr (CPT == 2 && sizeof(T) == 8) {
+      if (r_beg <= 1 && r_end >= HR)
+        sweep_c2d<HR, false, BC>(reinterpret_cast<const double*>(Ar), reinterpret_cast<const double*>(Br), col, 1,
+                                 HR, mc);
+      else
+        sweep_c2d<HR, true, BC>(reinterpret_cast<const double*>(Ar), reinterpret_cast<const double*>(Br), col, r_beg,
+                                r_end, mc);
+    } else if constexpr (CPT == 2) {
       if (r_beg <= 1 && r_end >= HR)
         sweep_c2<HR, false, BC>(reinterpret_cast<const float*>(Ar), reinterpret_cast<const float*>(Br), col, 1, HR,
                                 mc);
@@ -957,9 +1031,17 @@ size_t ws_bytes(int64_t n_videos, int n_frames, int h, int w) {
   return (size_t)n_videos * (n_frames - 1) * p.units * 10 * sizeof(double);
 }
 
+#ifndef CT_MOM_TWO_COL_F64
+#define CT_MOM_TWO_COL_F64 0
+#endif
 template <typename T, int BC>
 constexpr int cols_per_thread() {
-  return (sizeof(T) == 4 && kTwoColF32 && BC == 256) ? 2 : 1;
+  return (sizeof(T) == 4 && kTwoColF32 && BC == 256) ? 2 : (sizeof(T) == 8 && CT_MOM_TWO_COL_F64 && BC == 256) ? 2 : 1;
+}
+// the CTA-barrier kernel (plain-load fallback) runs fp64 one column per thread
+template <typename T, int BC>
+constexpr int cols_per_thread_sync() {
+  return sizeof(T) == 8 ? 1 : cols_per_thread<T, BC>();
 }
 
 // Kernel arguments and TMA map of one level; returns whether the frames admit
@@ -1009,10 +1091,11 @@ int launch_partials(const MomentArgs& a, const CUtensorMap& tmap, cudaStream_t s
     CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::total));
     kern<<<grid, BC / CPT, S::total, st>>>(a, tmap);
   } else {
-    using S = Smem<T, BR, NB, BC, BC / CPT>;
-    auto kern = ttc_moments_kernel<T, BR, NB, BC, CPT>;
+    constexpr int CPS = cols_per_thread_sync<T, BC>();
+    using S = Smem<T, BR, NB, BC, BC / CPS>;
+    auto kern = ttc_moments_kernel<T, BR, NB, BC, CPS>;
     CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::total));
-    kern<<<grid, BC / CPT, S::total, st>>>(a, tmap);
+    kern<<<grid, BC / CPS, S::total, st>>>(a, tmap);
   }
   return check_launch("ttc_moments");
 }
