@@ -320,6 +320,11 @@ def cfg5_sharded(quick: bool, world: int, rank: int):
     hbm, _ = load_peaks()
     n_est = nv_total * (nf - 1)
     bytes_ = n_est * 4 * 1080 * 1920
+    ext = [(1080, 1920)]
+    for _ in range(3):
+        ext.append((ext[-1][0] // 2, ext[-1][1] // 2))
+    pipe_bpf = 4 * (ext[0][0] * ext[0][1] + 4 * sum(hh * ww for hh, ww in ext[1:]))
+    pipe_bytes = nv_total * nf * pipe_bpf
     t = timed(max_level=3)
     t0 = timed(level=0)
     del fr
@@ -331,6 +336,13 @@ def cfg5_sharded(quick: bool, world: int, rank: int):
             "roofline": {"bound": "hbm", "achieved": bytes_ / t / 1e9 / world, "peak": hbm, "unit": "GB/s per GPU",
                          "frac": bytes_ / t / 1e9 / world / hbm,
                          "note": "whole pipeline (level-0 moments + block means, blurs, levels 1-3, epilogue)"},
+            "pipeline_traffic_roofline": {
+                "bound": "hbm", "bytes_per_frame": pipe_bpf, "achieved": pipe_bytes / t / 1e9 / world, "peak": hbm,
+                "unit": "GB/s per GPU", "frac": pipe_bytes / t / 1e9 / world / hbm,
+                "note": "HBM bytes the 4-level pipeline moves as designed: level-0 frames read once; per level "
+                        "l >= 1 the block means written and read once, the blurred level written and read once, "
+                        "and the next level's block means written: 4*(h0*w0 + 4*sum_l h_l*w_l) B per frame; "
+                        "band partials (< 0.5 %) not counted"},
             "level0_fused_kernel": {
                 "ms_per_step": t0 * 1e3, "est_s": n_est / t0,
                 "roofline": {"bound": "hbm", "achieved": bytes_ / t0 / 1e9 / world, "peak": hbm,
