@@ -527,6 +527,10 @@ __device__ __forceinline__ E warp_reduce10(const E (&o)[10], int lane, int& idx)
   return r5;
 }
 
+#ifndef CT_MOM_COMBINE_FIRST
+#define CT_MOM_COMBINE_FIRST 0  // probing: combine, then release (the round-1 order)
+#endif
+
 template <typename T, int BR, int NB, int BC, int NT>
 struct SmemWS {  // warp-streaming kernel: NB frame-band buffers + per-buffer / per-pair counters + warp partials
   static constexpr int NW = NT / 32;
@@ -692,6 +696,17 @@ __device__ __forceinline__ void moments_ws_body(const MomentArgs& a, const CUten
       if (last) __threadfence_block();
     }
     last = __shfl_sync(0xffffffffu, last, 0);
+#if !CT_MOM_COMBINE_FIRST
+    // frame p0 + i (buffer i % NB) is dead for this warp: the last warp to
+    // release it refills the buffer with frame p0 + i + NB.  Released before
+    // the combine: the last warp to deposit is usually the last to release,
+    // and the refill (one frame in flight) must not wait for its adds.  Slot
+    // i % NS stays intact: a warp reaches pair i + NS only after every warp
+    // released frame i + 1, i.e. after this warp's combine of pair i.
+    if (lane == 0) {
+      if ((atomicAdd(&rel[i % NB], 1) % NW) == NW - 1 && i + NB < nload) issue(i + NB);
+    }
+#endif
     if (last) {  // every warp has deposited for pair p: add the partials in warp order
       __syncwarp();
       if (lane < 10) {
@@ -703,12 +718,12 @@ __device__ __forceinline__ void moments_ws_body(const MomentArgs& a, const CUten
       }
     }
     __syncwarp();
-    // frame p0 + i (buffer i % NB) is dead for this warp: the last warp to
-    // release it refills the buffer with frame p0 + i + NB
+#if CT_MOM_COMBINE_FIRST
     if (lane == 0) {
       __threadfence_block();
       if ((atomicAdd(&rel[i % NB], 1) % NW) == NW - 1 && i + NB < nload) issue(i + NB);
     }
+#endif
   }
 }
 
