@@ -710,10 +710,16 @@ __device__ __forceinline__ void moments_ws_body(const MomentArgs& a, const CUten
     if (last) {  // every warp has deposited for pair p: add the partials in warp order
       __syncwarp();
       if (lane < 10) {
-        double acc = 0.0;
+        // the NW warp partials in a fixed pairwise tree (depth log2 NW: this
+        // warp's delay holds up every warp's next refill)
+        double t[NW];
 #pragma unroll
-        for (int w = 0; w < NW; ++w) acc += ps[w * 10 + lane];
-        acc *= 0.0625;  // undo the 4x stencil scaling of both factors
+        for (int w = 0; w < NW; ++w) t[w] = ps[w * 10 + lane];
+#pragma unroll
+        for (int h = 1; h < NW; h *= 2)
+#pragma unroll
+          for (int w = 0; w + h < NW; w += 2 * h) t[w] += t[w + h];
+        const double acc = t[0] * 0.0625;  // undo the 4x stencil scaling of both factors
         a.partials[((v * n_pairs + p) * a.units + unit) * 10 + lane] = (lane >= 6 && lane <= 8) ? -acc : acc;
       }
     }
