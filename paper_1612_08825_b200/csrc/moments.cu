@@ -690,12 +690,30 @@ __device__ __forceinline__ void moments_ws_body(const MomentArgs& a, const CUten
     if ((lane & 1) == 0 && idx >= 0) ps[wid * 10 + idx] = wsum;
     __syncwarp();
     int last = 0;
-    if (lane == 0) {
-      __threadfence_block();
-      last = (atomicAdd(&cnt[slot], 1) % NW) == NW - 1;
-      if (last) __threadfence_block();
+#if !CT_MOM_COMBINE_FIRST
+    if constexpr (S::NS == NB) {
+      // one counter per pair slot: depositing for pair i and releasing frame i
+      // (buffer i % NB) happen at the same point, so the last warp to arrive
+      // both issues the refill and combines the pair
+      if (lane == 0) {
+        __threadfence_block();
+        last = (atomicAdd(&cnt[slot], 1) % NW) == NW - 1;
+        if (last) {
+          __threadfence_block();
+          if (i + NB < nload) issue(i + NB);
+        }
+      }
+      last = __shfl_sync(0xffffffffu, last, 0);
+    } else
+#endif
+    {
+      if (lane == 0) {
+        __threadfence_block();
+        last = (atomicAdd(&cnt[slot], 1) % NW) == NW - 1;
+        if (last) __threadfence_block();
+      }
+      last = __shfl_sync(0xffffffffu, last, 0);
     }
-    last = __shfl_sync(0xffffffffu, last, 0);
 #if !CT_MOM_COMBINE_FIRST
     // frame p0 + i (buffer i % NB) is dead for this warp: the last warp to
     // release it refills the buffer with frame p0 + i + NB.  Released before
@@ -703,8 +721,10 @@ __device__ __forceinline__ void moments_ws_body(const MomentArgs& a, const CUten
     // and the refill (one frame in flight) must not wait for its adds.  Slot
     // i % NS stays intact: a warp reaches pair i + NS only after every warp
     // released frame i + 1, i.e. after this warp's combine of pair i.
-    if (lane == 0) {
-      if ((atomicAdd(&rel[i % NB], 1) % NW) == NW - 1 && i + NB < nload) issue(i + NB);
+    if constexpr (S::NS != NB) {
+      if (lane == 0) {
+        if ((atomicAdd(&rel[i % NB], 1) % NW) == NW - 1 && i + NB < nload) issue(i + NB);
+      }
     }
 #endif
     if (last) {  // every warp has deposited for pair p: add the partials in warp order
