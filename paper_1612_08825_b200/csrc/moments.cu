@@ -26,8 +26,9 @@
 //   * Per pair the 256 per-thread sums become one partial per band: in the
 //     warp-streaming kernel (ttc_moments_ws_kernel, used whenever the frames
 //     admit a TMA map) each warp reduces its lanes with a transpose-reduce
-//     butterfly and the last warp to deposit adds the warp partials in warp
-//     order, with no CTA barrier; the CTA-barrier kernel (ttc_moments_kernel,
+//     butterfly and deposits one partial; two pairs later (when the frame ring
+//     guarantees every warp has deposited) one warp, rotating, adds them in a
+//     fixed tree, with no CTA barrier; the CTA-barrier kernel (ttc_moments_kernel,
 //     LDG loader for frames without a TMA map) reduces through shared memory
 //     in a fixed tree.  moments_finalize adds the band partials in a fixed
 //     order.  Results are bit-reproducible and independent of how pairs are
@@ -527,20 +528,16 @@ __device__ __forceinline__ E warp_reduce10(const E (&o)[10], int lane, int& idx)
   return r5;
 }
 
-#ifndef CT_MOM_COMBINE_FIRST
-#define CT_MOM_COMBINE_FIRST 0  // probing: combine, then release (the round-1 order)
-#endif
-
 template <typename T, int BR, int NB, int BC, int NT>
-struct SmemWS {  // warp-streaming kernel: NB frame-band buffers + per-buffer / per-pair counters + warp partials
+struct SmemWS {  // warp-streaming kernel: NB frame-band buffers + per-buffer release counters + warp partials
   static constexpr int NW = NT / 32;
-  static constexpr int NS = 3;  // pair slots for the warp partials (2 suffice, see the kernel)
+  // pair slots for the warp partials: pairs i - (NB - 1) .. i + NB - 2 can be live (see the kernel)
+  static constexpr int NS = 2 * NB - 2 > 3 ? 2 * NB - 2 : 3;
   static constexpr size_t buf_elems = (size_t)(BR + 1) * BC + 8;
   static constexpr size_t buf_bytes = (buf_elems * sizeof(T) + 127) & ~size_t(127);
   static constexpr size_t bars_off = NB * buf_bytes;
   static constexpr size_t rel_off = bars_off + 8 * NB;
-  static constexpr size_t cnt_off = rel_off + 4 * NB;
-  static constexpr size_t part_off = (cnt_off + 4 * NS + 15) & ~size_t(15);
+  static constexpr size_t part_off = (rel_off + 4 * NB + 15) & ~size_t(15);
   static constexpr size_t total = part_off + (size_t)NS * NW * 10 * sizeof(double);
 };
 
@@ -551,14 +548,17 @@ struct SmemWS {  // warp-streaming kernel: NB frame-band buffers + per-buffer / 
 //     release counter, and the last of the NW warps to release it issues the
 //     TMA of frame i + NB into the freed buffer.
 //   * A warp's 32 lanes reduce their ten sums with warp_reduce10 and deposit
-//     one 10-value partial per warp in a pair slot; the last warp to deposit
-//     for a pair adds the NW partials in warp order and writes the band's
-//     partial (same layout as the CTA-reduced kernel; the add order is fixed,
-//     so results stay bit-reproducible).
-//   * A warp can run at most NB - 1 pairs ahead of the slowest one (it waits
-//     for frame i + 1, which is only loaded once every warp released frame
-//     i + 1 - NB, after depositing for pair i + 1 - NB), so pair slot i % NS
-//     (NS >= 2) is never reused before its combine has run.
+//     one 10-value partial per warp in pair slot i % NS.  Pair i - (NB - 1)
+//     is complete once a warp holds frame i + 1 (that load waited for every
+//     warp's release of frame i + 1 - NB, which follows its deposit), so warp
+//     (i - (NB - 1)) % NW adds its NW partials in a fixed pairwise tree and
+//     writes the band's partial; the last NB - 1 pairs are combined after a
+//     barrier at the end.  The add order is fixed: results are
+//     bit-reproducible.  No arrival counter is needed and the combine rotates
+//     over the warps instead of delaying the slowest one (each per-pair delay
+//     of one warp holds up every warp's next refill: counter-based combining
+//     by the last arriver was 1.3 % slower on cfg2).
+//   * Pairs i - (NB - 1) .. i + NB - 2 can hold live partials, so NS = 2 NB - 2.
 //   * RS row splits: the 32 / RS lanes of a warp's row group own consecutive
 //     column groups (CPT columns each) and the RS groups split the band rows,
 //     so fp32 bands run 256 threads (16 warps per SM) with two columns per
@@ -592,7 +592,6 @@ __device__ __forceinline__ void moments_ws_body(const MomentArgs& a, const CUten
   auto buf = [&](int k) { return reinterpret_cast<T*>(smem + (size_t)k * S::buf_bytes); };
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::bars_off);
   int* rel = reinterpret_cast<int*>(smem + S::rel_off);
-  int* cnt = reinterpret_cast<int*>(smem + S::cnt_off);
   double* part = reinterpret_cast<double*>(smem + S::part_off);
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -633,13 +632,27 @@ __device__ __forceinline__ void moments_ws_body(const MomentArgs& a, const CUten
       mbar_init(&bars[i], 1);
       rel[i] = 0;
     }
-    for (int i = 0; i < S::NS; ++i) cnt[i] = 0;
     mbar_fence_init();
   }
   __syncthreads();
   if (tid == 0)
     for (int f = 0; f < min(NB, nload); ++f) issue(f);
 
+  // band partial of pair p0 + j: the NW warp partials in a fixed pairwise tree
+  auto combine = [&](int j) {
+    const double* pj = part + (size_t)(j % S::NS) * NW * 10;
+    if (lane < 10) {
+      double t[NW];
+#pragma unroll
+      for (int w = 0; w < NW; ++w) t[w] = pj[w * 10 + lane];
+#pragma unroll
+      for (int h = 1; h < NW; h *= 2)
+#pragma unroll
+        for (int w = 0; w + h < NW; w += 2 * h) t[w] += t[w + h];
+      const double acc = t[0] * 0.0625;  // undo the 4x stencil scaling of both factors
+      a.partials[((v * n_pairs + p0 + j) * a.units + unit) * 10 + lane] = (lane >= 6 && lane <= 8) ? -acc : acc;
+    }
+  };
   for (int i = 0; i < p1 - p0; ++i) {
     const int p = p0 + i;
     mbar_wait(&bars[i % NB], (uint32_t)((i / NB) & 1));
@@ -685,72 +698,27 @@ __device__ __forceinline__ void moments_ws_body(const MomentArgs& a, const CUten
     thread_sums<ACC, CPT, E, kRaw, HR>(mc, in_col, xc, yc0, o);
     int idx;
     const double wsum = (double)warp_reduce10<E>(o, lane, idx);
-    const int slot = i % S::NS;
-    double* ps = part + (size_t)slot * NW * 10;
+    double* ps = part + (size_t)(i % S::NS) * NW * 10;
     if ((lane & 1) == 0 && idx >= 0) ps[wid * 10 + idx] = wsum;
-    __syncwarp();
-    int last = 0;
-#if !CT_MOM_COMBINE_FIRST
-    if constexpr (S::NS == NB) {
-      // one counter per pair slot: depositing for pair i and releasing frame i
-      // (buffer i % NB) happen at the same point, so the last warp to arrive
-      // both issues the refill and combines the pair
-      if (lane == 0) {
-        __threadfence_block();
-        last = (atomicAdd(&cnt[slot], 1) % NW) == NW - 1;
-        if (last) {
-          __threadfence_block();
-          if (i + NB < nload) issue(i + NB);
-        }
-      }
-      last = __shfl_sync(0xffffffffu, last, 0);
-    } else
-#endif
-    {
-      if (lane == 0) {
-        __threadfence_block();
-        last = (atomicAdd(&cnt[slot], 1) % NW) == NW - 1;
-        if (last) __threadfence_block();
-      }
-      last = __shfl_sync(0xffffffffu, last, 0);
+    // Pair i - (NB - 1) is complete: frame i + 1 (awaited above) was loaded
+    // only after every warp released frame i + 1 - NB, which each warp does
+    // after depositing that pair.  Its combine rotates over the warps, so no
+    // arrival counter is needed and the slowest warp carries no extra work.
+    if (i >= NB - 1 && wid == (i - (NB - 1)) % NW) {
+      __threadfence_block();
+      combine(i - (NB - 1));
     }
-#if !CT_MOM_COMBINE_FIRST
+    __syncwarp();
     // frame p0 + i (buffer i % NB) is dead for this warp: the last warp to
-    // release it refills the buffer with frame p0 + i + NB.  Released before
-    // the combine: the last warp to deposit is usually the last to release,
-    // and the refill (one frame in flight) must not wait for its adds.  Slot
-    // i % NS stays intact: a warp reaches pair i + NS only after every warp
-    // released frame i + 1, i.e. after this warp's combine of pair i.
-    if constexpr (S::NS != NB) {
-      if (lane == 0) {
-        if ((atomicAdd(&rel[i % NB], 1) % NW) == NW - 1 && i + NB < nload) issue(i + NB);
-      }
-    }
-#endif
-    if (last) {  // every warp has deposited for pair p: add the partials in warp order
-      __syncwarp();
-      if (lane < 10) {
-        // the NW warp partials in a fixed pairwise tree (depth log2 NW: this
-        // warp's delay holds up every warp's next refill)
-        double t[NW];
-#pragma unroll
-        for (int w = 0; w < NW; ++w) t[w] = ps[w * 10 + lane];
-#pragma unroll
-        for (int h = 1; h < NW; h *= 2)
-#pragma unroll
-          for (int w = 0; w + h < NW; w += 2 * h) t[w] += t[w + h];
-        const double acc = t[0] * 0.0625;  // undo the 4x stencil scaling of both factors
-        a.partials[((v * n_pairs + p) * a.units + unit) * 10 + lane] = (lane >= 6 && lane <= 8) ? -acc : acc;
-      }
-    }
-    __syncwarp();
-#if CT_MOM_COMBINE_FIRST
+    // release it refills the buffer with frame p0 + i + NB
     if (lane == 0) {
       __threadfence_block();
       if ((atomicAdd(&rel[i % NB], 1) % NW) == NW - 1 && i + NB < nload) issue(i + NB);
     }
-#endif
   }
+  // the last NB - 1 pairs
+  __syncthreads();
+  for (int j = max(0, p1 - p0 - (NB - 1)) + wid; j < p1 - p0; j += NW) combine(j);
 }
 
 template <typename T, int BR, int NB, int BC, int CPT, int RS>
