@@ -216,7 +216,7 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
-DP_PER_PX = 722.086e6 * 32 / (256 * 63 * 255 * 255)  # ncu FP64 warp instructions x 32 lanes per grid pixel (22.0)
+DP_PER_PX = 711.539e6 * 32 / (256 * 63 * 255 * 255)  # ncu FP64 warp instructions x 32 lanes per grid pixel (21.7)
 FP64_LANE_PEAK = 32.2e12 / 2
 
 
@@ -440,7 +440,7 @@ def main():
             "kernel_ms": t_k * 1e3, "step_ms": dt / args.steps * 1e3,
             "kernel_timing": "CUDA events around ct_ttc_moments in every timed step, on its stream, max over ranks",
             # the kernel is FP64-issue bound (profiles/r01_ttc_moments_ws_f64_cfg2.txt):
-            # 722.1 M FP64 warp instructions per 256-video launch = 21.86 per thread-pixel
+            # 711.5 M FP64 warp instructions per 256-video launch = 21.7 per thread-pixel
             # (sweep 20 + 7/16 band-halo row + the per-pair epilogue and warp reduction)
             "fp64_pipe": {"dp_instr_per_grid_px": DP_PER_PX,
                           "achieved_lane_ops_per_s": DP_PER_PX * V * (NFRAMES - 1) * 255 * 255 / t_k,
