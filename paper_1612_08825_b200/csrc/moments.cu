@@ -567,7 +567,7 @@ struct SmemWS {  // warp-streaming kernel: NB frame-band buffers + per-buffer re
 #define CT_MOM_MINB64 0
 #endif
 #ifndef CT_MOM_MINB32
-#define CT_MOM_MINB32 4
+#define CT_MOM_MINB32 3
 #endif
 // resident CTAs per SM the register budget is sized for (fp32: CT_MOM_MINB32, see band_rows)
 template <typename T, int BC, int RS>
@@ -959,13 +959,13 @@ inline unsigned finalize_grid(int64_t n_sys) {
 }
 
 // Band height: 16 rows for f64 (3 x 35 KB buffers, 2 CTAs/SM, FP64-bound);
-// 16 rows for f32 (3 x 17 KB, 4 CTAs/SM of 4 warps with <= 128 registers):
-// the fp32 kernel is latency-bound; once the per-pair work left the slowest
-// warp (rotating combine), 16 warps/SM with 16-row bands beat 12 warps/SM with
-// 20- or 22-row bands on the cfg5 pipeline (0.564 -> 0.555 ms per 128-frame
-// video); 4-deep rings lose (profiles/r01_moments_probe.md).
+// 20 rows for f32 (3 x 21 KB, 3 CTAs/SM of 4 warps with <= 170 registers):
+// the fp32 kernel is latency-bound; on the full cfg5 stream 20-row bands at
+// 12 warps/SM match 22 rows and beat 16-row bands at 4 CTAs/SM (which win on
+// a single 128-frame video), 32-row bands at 8 warps/SM and 4-deep rings
+// (profiles/r01_moments_probe.md).
 #ifndef CT_MOM_BR32
-#define CT_MOM_BR32 16
+#define CT_MOM_BR32 20
 #endif
 #ifndef CT_MOM_NB32
 #define CT_MOM_NB32 3
