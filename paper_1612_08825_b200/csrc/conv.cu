@@ -617,6 +617,9 @@ int launch_tma3d(const TileArgs& a0, const T* taps_host, int ntaps, cudaStream_t
 // taps come from the parameter bank with a uniform offset, and each staged
 // value feeds NZ * TY * NW FMAs.  Per output the taps are still applied in
 // row-major (j0, j1, j2) order from 0.0, so fp64 results are bit-exact.
+#ifndef CT_ZW_WARP_REL
+#define CT_ZW_WARP_REL 1  // per-warp stage release (0: CTA barrier per slice, the round-1 kernel)
+#endif
 template <typename T, int NZ, int NH, int NW, int TY, int VX, int LW, int MAXT>
 __global__ void __launch_bounds__(MAXT, 1) xcorr_zwalk(const TileArgs a, const __grid_constant__ TapsParam<T> taps,
                                                       const __grid_constant__ CUtensorMap tmap, int pxa,
@@ -635,6 +638,10 @@ __global__ void __launch_bounds__(MAXT, 1) xcorr_zwalk(const TileArgs a, const _
   const size_t stage_bytes = ((size_t)a.sx * a.sy * sizeof(T) + 127) & ~size_t(127);
   auto stage = [&](int s) { return reinterpret_cast<T*>(smem_zw + (size_t)s * stage_bytes); };
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_zw + NS * stage_bytes);
+#if CT_ZW_WARP_REL
+  int* rel = reinterpret_cast<int*>(smem_zw + NS * stage_bytes + 8 * NS);  // per-stage release counters
+  const int nwarps = (int)(blockDim.x >> 5), lane = tid & 31;
+#endif
   const uint32_t box_bytes = (uint32_t)(a.sx * a.sy * sizeof(T));
   const bool active = ty < a.tyn;
   const int64_t total = a.batch * tiles_y * tiles_x * (int64_t)a.oz;
@@ -642,6 +649,9 @@ __global__ void __launch_bounds__(MAXT, 1) xcorr_zwalk(const TileArgs a, const _
   const int64_t end = min(total, pos + per_cta);
   if (tid == 0) {
     for (int i = 0; i < NS; ++i) mbar_init(&bars[i], 1);
+#if CT_ZW_WARP_REL
+    for (int i = 0; i < NS; ++i) rel[i] = 0;
+#endif
     mbar_fence_init();
   }
   __syncthreads();
@@ -661,8 +671,8 @@ __global__ void __launch_bounds__(MAXT, 1) xcorr_zwalk(const TileArgs a, const _
     const int g_lo = max(0, s_beg), g_hi = min(a.mz, s_end);
     const int nsl = max(0, g_hi - g_lo);
     const int g0 = gcount;
-    auto issue = [&](int k) {
-      if (tid == 0) {
+    auto issue = [&](int k, bool any = false) {
+      if (any || tid == 0) {
         const int st = (g0 + k) % NS;
         fence_proxy_async_smem();
         mbar_arrive_expect_tx(&bars[st], box_bytes);
@@ -732,8 +742,18 @@ __global__ void __launch_bounds__(MAXT, 1) xcorr_zwalk(const TileArgs a, const _
             }
           }
         }
+#if CT_ZW_WARP_REL
+        // stage consumed by this warp: the last warp to release it refills
+        // it (no CTA barrier per slice; warps drift by up to NS - 1 slices)
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence_block();
+          if ((atomicAdd(&rel[g % NS], 1) % nwarps) == nwarps - 1 && k + NS < nsl) issue(k + NS, true);
+        }
+#else
         __syncthreads();  // stage consumed
         if (k + NS < nsl) issue(k + NS);
+#endif
       }
       // slot NZ-1 now holds output z = s + pz - (NZ-1), complete
       const int zo = s + a.pz - (NZ - 1);
@@ -760,6 +780,9 @@ __global__ void __launch_bounds__(MAXT, 1) xcorr_zwalk(const TileArgs a, const _
         for (int x = 0; x < VX; ++x) acc[0][yi][x] = T(0);
     }
     gcount += nsl;
+#if CT_ZW_WARP_REL
+    __syncthreads();  // run boundary: every stage free before the next run's first loads
+#endif
   }
 }
 
