@@ -655,7 +655,7 @@ __device__ __forceinline__ void moments_ws_body(const MomentArgs& a, const CUten
   };
   for (int i = 0; i < p1 - p0; ++i) {
     const int p = p0 + i;
-    mbar_wait(&bars[i % NB], (uint32_t)((i / NB) & 1));
+    if (i == 0) mbar_wait(&bars[0], 0u);  // later pairs: frame i arrived as frame B of pair i - 1
     mbar_wait(&bars[(i + 1) % NB], (uint32_t)(((i + 1) / NB) & 1));
     const T* A = buf(i % NB);
     const T* B = buf((i + 1) % NB);
