@@ -22,7 +22,19 @@ from .conv import (
     xcorr_direct,
 )
 from .kernels import KERNELS, GradientField, NamedKernel, gradient, kernel_lookup
-from .synth import SynthConfig, approach_stream, generate, make_texture, make_textures, zoom_frames
+from .synth import (
+    ScoreReport,
+    SynthConfig,
+    SyntheticSequence,
+    approach_stream,
+    generate,
+    make_texture,
+    make_texture_device,
+    make_textures,
+    score_mse,
+    zoom_frame,
+    zoom_frames,
+)
 from .ttc import (
     TRACE_HEADER,
     FramePair,

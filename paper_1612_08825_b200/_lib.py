@@ -120,16 +120,16 @@ def to_device(x, keep_f32: bool = True) -> tuple[torch.Tensor, bool]:
     """Coerce an array-like to a contiguous CUDA tensor.
 
     Returns (tensor, was_numpy).  numpy / lists are coerced to float64 as the
-    reference does (conv.py:101-102, ttc.py:293); CUDA tensors keep float32 or
-    float64 (the fp32 path) and other dtypes become float64.
+    reference does (conv.py:101-102, ttc.py:293), and so are host (CPU) torch
+    tensors; only CUDA tensors keep float32 (the fp32 path) -- other dtypes
+    become float64.
     """
     if isinstance(x, torch.Tensor):
         t = x
+        if not t.is_cuda:  # host tensors are coerced like numpy input (float64)
+            return t.to(device="cuda", dtype=torch.float64).contiguous(), True
         if t.dtype not in (torch.float32, torch.float64) or (t.dtype == torch.float32 and not keep_f32):
             t = t.to(torch.float64)
-        if not t.is_cuda:
-            t = t.to("cuda")
-            return t.contiguous(), True
         return t.contiguous(), False
     a = np.ascontiguousarray(x, dtype=np.float64)
     return torch.from_numpy(a).to("cuda", non_blocking=False), True

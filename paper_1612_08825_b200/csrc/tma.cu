@@ -28,7 +28,9 @@ bool encode_tmap_2d(CUtensorMap* map, const void* base, int esz, uint64_t cols, 
   if ((reinterpret_cast<uintptr_t>(base) & 15) != 0) return false;
   if ((cols * esz) % 16 != 0) return false;
   if ((box_cols * esz) % 16 != 0 || box_cols > 256 || box_rows > 256) return false;
-  if (rows >= (1ull << 32) || cols >= (1ull << 32)) return false;
+  // TMA tensor coordinates are signed 32-bit: callers pass row indices as int,
+  // so a taller view must fall back to the plain-load kernels
+  if (rows >= (1ull << 31) || cols >= (1ull << 31)) return false;
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {cols, rows};
@@ -46,6 +48,7 @@ bool encode_tmap_3d(CUtensorMap* map, const void* base, int esz, uint64_t d0, ui
                     uint32_t box0, uint32_t box1) {
   if ((reinterpret_cast<uintptr_t>(base) & 15) != 0) return false;
   if ((d0 * esz) % 16 != 0 || (box0 * esz) % 16 != 0 || box0 > 256 || box1 > 256) return false;
+  if (d0 >= (1ull << 31) || d1 >= (1ull << 31) || d2 >= (1ull << 31)) return false;  // s32 coordinates
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[3] = {d0, d1, d2};
@@ -63,6 +66,7 @@ bool encode_tmap_4d(CUtensorMap* map, const void* base, int esz, uint64_t d0, ui
                     uint32_t box0, uint32_t box1) {
   if ((reinterpret_cast<uintptr_t>(base) & 15) != 0) return false;
   if ((d0 * esz) % 16 != 0 || (box0 * esz) % 16 != 0 || box0 > 256 || box1 > 256) return false;
+  if (d0 >= (1ull << 31) || d1 >= (1ull << 31) || d2 >= (1ull << 31) || d3 >= (1ull << 31)) return false;
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[4] = {d0, d1, d2, d3};

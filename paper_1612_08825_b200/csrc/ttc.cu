@@ -1083,9 +1083,15 @@ extern "C" int ct_ttc_multiscale_select(const double* est_levels, int64_t count,
   return check_launch("multiscale_select");
 }
 
+// multiscale: the reference accepts any max_level (its walk stops once the
+// extents drop below 4, ttc.py:264-279) and ignores `level`; extents < 2^30
+// stop the walk long before kMaxPyr levels
+static int clamp_max_level(int max_level) { return std::min(max_level, kMaxPyr - 1); }
+
 extern "C" size_t ct_run_sequence_workspace_bytes(int dtype, int64_t n_videos, int64_t n_frames, int64_t h, int64_t w,
                                                   int level, int max_level) {
   if (n_frames < 2 || h < 1 || w < 1) return 0;
+  max_level = clamp_max_level(max_level);
   if (dtype == CT_F64) return run_seq_ws<double>(n_videos, (int)n_frames, (int)h, (int)w, level, max_level);
   return run_seq_ws<float>(n_videos, (int)n_frames, (int)h, (int)w, level, max_level);
 }
@@ -1096,14 +1102,13 @@ static int check_run_seq_args(int64_t n_frames, int64_t h, int64_t w, int level,
   if (max_level < 0) {
     CT_REQUIRE(level >= 0, "level must be >= 0");
     int64_t lh = h, lw = w;
-    for (int i = 0; i < level; ++i) {
+    for (int i = 0; i < level && lh >= 4 && lw >= 4; ++i) {
       lh /= 2;
       lw /= 2;
     }
     CT_REQUIRE(lh >= 4 && lw >= 4, "extents (%lld, %lld) leave (%lld, %lld) after %d halvings, need >= 4",
                (long long)h, (long long)w, (long long)lh, (long long)lw, level);
   }
-  CT_REQUIRE(max_level < 31 && level < 31, "level too large");
   return CT_OK;
 }
 
@@ -1114,6 +1119,7 @@ extern "C" int ct_run_sequence(int dtype, const void* frames, int64_t n_videos, 
   CT_DT_CHECK(dtype);
   int rc = check_run_seq_args(n_frames, h, w, level, max_level);
   if (rc) return rc;
+  max_level = clamp_max_level(max_level);
   cudaStream_t st = as_stream(stream);
   if (dtype == CT_F64)
     return run_seq<double>((const double*)frames, n_videos, (int)n_frames, (int)h, (int)w, level, max_level, c_min,

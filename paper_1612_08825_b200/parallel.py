@@ -58,6 +58,15 @@ def shard_pairs(n_frames: int, world: int) -> list[PairShard]:
     return out
 
 
+def collective_device(group=None) -> torch.device:
+    """Where tensors must live for this group's collectives: the current CUDA
+    device under NCCL, the host under gloo (CUDA results are staged through
+    host memory there; gloo is the CPU test backend)."""
+    if dist.is_initialized() and dist.get_backend(group) == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
 def _default_compute(frames_local, level, max_level, c_min):
     from .ttc import run_sequence_batch
     t = frames_local if isinstance(frames_local, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(frames_local))
@@ -71,7 +80,9 @@ def run_sequence_sharded(frames, level=0, max_level=None, c_min=1e-9, group=None
     ``frames`` is either the whole stack (each rank slices its shard) or, with
     frames_are_local=True, this rank's shard frames p0..p1 already (then pass
     n_frames, the global frame count).  Every rank returns the full, ordered
-    result (gathered with one all_gather; rows identical to the 1-GPU run).
+    result (gathered with one all_gather; rows identical to the 1-GPU run) on
+    collective_device(group): the GPU under NCCL, the host under gloo.
+    Ranks beyond the pair count compute nothing and still join the gather.
     """
     compute = compute or _default_compute
     world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -85,11 +96,12 @@ def run_sequence_sharded(frames, level=0, max_level=None, c_min=1e-9, group=None
     if me.n_pairs > 0:
         rows = compute(local, level, max_level, c_min)
         rows = torch.as_tensor(rows, dtype=torch.float64)
-    else:
+    else:  # more ranks than pairs: this rank only takes part in the gather
         rows = torch.empty((0, 10), dtype=torch.float64)
     if world == 1:
         return rows
-    dev = rows.device
+    dev = collective_device(group)
+    rows = rows.to(dev)
     width = max(s.n_pairs for s in plan)
     buf = torch.full((width, 10), float("nan"), dtype=torch.float64, device=dev)
     buf[:me.n_pairs] = rows
@@ -141,6 +153,8 @@ def exchange_halo(local_in: torch.Tensor, plan: list[RowSlab], rank: int, pl0: i
     neighbours' rows (batched point-to-point).  Returns (rows, first_row)."""
     me = plan[rank]
     lo, hi = needed_rows(me, pl0, n0, m0)
+    home = local_in.device
+    local_in = local_in.to(collective_device(group))  # gloo: stage CUDA rows through the host
     ops, recv = [], []
     for other in plan:
         # rows `other` needs from me
@@ -161,7 +175,7 @@ def exchange_halo(local_in: torch.Tensor, plan: list[RowSlab], rank: int, pl0: i
     pieces = [(a, t) for a, t in pieces if t.shape[0] > 0]
     pieces.sort(key=lambda p: p[0])
     rows = torch.cat([t for _, t in pieces]) if pieces else local_in[:0]
-    return rows, lo
+    return rows.to(home), lo
 
 
 def xcorr_rows_sharded(local_in: torch.Tensor, m0: int, kernel, shape_mode: str = "full", group=None,

@@ -7,9 +7,11 @@ Mirrors convtact.synth (/root/reference/pkg/src/convtact/synth.py):
     a min-max rescale (synth.py:68-85);
   * zoom frames: separable Catmull-Rom magnification about the FOE, done by
     ct_zoom_frames (synth.py:88-126), bit-identical in float64;
-  * generate(SynthConfig): frames t = 0..frames-1 with magnification
-    t0 / (t0 - t) (synth.py:129-143); sensor noise from the independent
-    PCG64(SeedSequence([seed, 1])) stream when noise_sigma > 0.
+  * generate(SynthConfig) -> SyntheticSequence(frames, truth, config):
+    frames t = 0..frames-1 with magnification t0 / (t0 - t)
+    (synth.py:129-143); sensor noise from the independent
+    PCG64(SeedSequence([seed, 1])) stream when noise_sigma > 0;
+  * score_mse: the trace-vs-truth MSE report (synth.py:186-208).
 
 approach_stream() implements the long-video rule used for BASELINE config 5
 (SURVEY.md D3): the reference forbids frames >= t0, so a 1024-frame stream is
@@ -19,6 +21,7 @@ T0 ~ U[50, 500], cut while the true time to contact is still >= 20 frames.
 
 from __future__ import annotations
 
+import csv
 import ctypes
 import math
 from dataclasses import dataclass
@@ -62,7 +65,7 @@ class SynthConfig:
         return self.foe[0] * self.width, self.foe[1] * self.height
 
 
-def make_texture(width: int, height: int, seed: int, device="cuda") -> torch.Tensor:
+def make_texture_device(width: int, height: int, seed: int, device="cuda") -> torch.Tensor:
     """Band-limited random texture in [0, 1] as a float64 CUDA tensor (synth.py:68-85)."""
     if width < 16 or height < 16:
         raise ValueError(f"texture {width}x{height} too small, need >= 16")
@@ -74,6 +77,12 @@ def make_texture(width: int, height: int, seed: int, device="cuda") -> torch.Ten
     if not bool(hi > lo):
         return torch.zeros_like(img)
     return (img - lo) / (hi - lo)
+
+
+def make_texture(width: int, height: int, seed: int) -> np.ndarray:
+    """synth.make_texture (synth.py:68-85): the texture as a float64 numpy array
+    (computed on the device; make_texture_device keeps it there)."""
+    return make_texture_device(width, height, seed).cpu().numpy()
 
 
 def make_textures(width: int, height: int, seeds, device="cuda") -> torch.Tensor:
@@ -111,9 +120,34 @@ def zoom_frames(texture: torch.Tensor, foe_px, mags, dtype=torch.float64, out: t
     return out
 
 
-def generate(cfg: SynthConfig, dtype=torch.float64) -> tuple[torch.Tensor, np.ndarray]:
-    """(frames [frames, h, w] on the device, truth rows (frame, ttc, foe_x, foe_y)) (synth.py:129-143)."""
-    tex = make_texture(cfg.width, cfg.height, cfg.seed)
+def zoom_frame(texture, foe_px, magnification: float):
+    """synth.zoom_frame (synth.py:110-126): magnify about foe_px with edge
+    clamping, on the device.  numpy in -> numpy out; a CUDA tensor stays."""
+    if magnification < 1.0:
+        raise ValueError(f"magnification must be >= 1, got {magnification}")
+    on_dev = isinstance(texture, torch.Tensor) and texture.is_cuda
+    tex = texture.to(torch.float64) if on_dev else torch.from_numpy(np.ascontiguousarray(texture, dtype=np.float64)).cuda()
+    out = zoom_frames(tex, foe_px, [float(magnification)])[0]
+    return out if on_dev else out.cpu().numpy()
+
+
+@dataclass(frozen=True)
+class SyntheticSequence:
+    """synth.SyntheticSequence (synth.py:61-65).  ``frames`` is a numpy array
+    from generate(cfg) and a CUDA tensor from generate(cfg, device=True)."""
+
+    frames: object
+    truth: np.ndarray  # rows (frame, ttc, foe_x, foe_y), FOE in array pixels
+    config: SynthConfig
+
+
+def generate(cfg: SynthConfig, device: bool = False, dtype=torch.float64) -> SyntheticSequence:
+    """synth.generate (synth.py:129-143) with the frames zoomed on the device.
+
+    Default: the reference's result, frames a float64 numpy array.  With
+    device=True the frames stay on the GPU as a ``dtype`` CUDA tensor
+    (rounded from float64; the benchmark / test input path)."""
+    tex = make_texture_device(cfg.width, cfg.height, cfg.seed)
     mags = [cfg.t0 / (cfg.t0 - t) for t in range(cfg.frames)]
     frames = zoom_frames(tex, cfg.foe_px, mags, dtype=torch.float64)
     if cfg.noise_sigma > 0:
@@ -122,8 +156,49 @@ def generate(cfg: SynthConfig, dtype=torch.float64) -> tuple[torch.Tensor, np.nd
             noise = torch.from_numpy(noise_rng.normal(0.0, cfg.noise_sigma, (cfg.height, cfg.width))).to(frames.device)
             frames[t] = torch.clamp(frames[t] + noise, 0.0, 1.0)
     fx, fy = cfg.foe_px
-    truth = np.array([(t, cfg.t0 - t, fx, fy) for t in range(cfg.frames)], dtype=np.float64)
-    return frames.to(dtype), truth
+    truth = np.array([(t, cfg.t0 - t, fx, fy) for t in range(cfg.frames)], dtype=np.float64).reshape(-1, 4)
+    out = frames.to(dtype) if device else frames.cpu().numpy()
+    return SyntheticSequence(frames=out, truth=truth, config=cfg)
+
+
+@dataclass(frozen=True)
+class ScoreReport:
+    mse: float
+    compared: int
+    excluded: int
+
+
+def _read_ttc_column(path):  # synth.py:172-183
+    with open(path, newline="") as f:
+        reader = csv.DictReader(f)
+        if reader.fieldnames is None or "frame" not in reader.fieldnames or "ttc" not in reader.fieldnames:
+            raise ValueError(f"{path}: need a CSV with frame and ttc columns")
+        rows = {}
+        for rec in reader:
+            rows[int(rec["frame"])] = (float(rec["ttc"]),
+                                       rec.get("degenerate", "false").strip().lower() == "true")
+    return rows
+
+
+def score_mse(pred_path, truth_path) -> ScoreReport:
+    """synth.score_mse (synth.py:186-208): MSE of predicted vs true ttc over the
+    shared frame indices; degenerate / non-finite predictions are excluded but
+    counted.  Host CSV bookkeeping (a trace from write_trace against truth.csv)."""
+    pred = _read_ttc_column(pred_path)
+    truth = _read_ttc_column(truth_path)
+    shared = sorted(set(pred) & set(truth))
+    if not shared:
+        raise ValueError("prediction and truth share no frame indices")
+    errs, excluded = [], 0
+    for idx in shared:
+        p, degenerate = pred[idx]
+        if degenerate or not math.isfinite(p):
+            excluded += 1
+            continue
+        errs.append((p - truth[idx][0]) ** 2)
+    if not errs:
+        raise ValueError("no comparable rows: every prediction was degenerate or non-finite")
+    return ScoreReport(mse=float(np.mean(errs)), compared=len(errs), excluded=excluded)
 
 
 @dataclass(frozen=True)
@@ -166,7 +241,7 @@ def approach_stream(frames: int, height: int, width: int, seed: int, dtype=torch
     truth = np.empty(frames)
     foe_px = (foe[0] * width, foe[1] * height)
     for s in approach_segments(frames, seed):
-        tex = make_texture(width, height, s.texture_seed)
+        tex = make_texture_device(width, height, s.texture_seed)
         mags = [s.t0 / (s.t0 - t) for t in range(s.length)]
         zoom_frames(tex, foe_px, mags, dtype=dtype, out=out[s.start:s.start + s.length])
         truth[s.start:s.start + s.length] = [s.t0 - t for t in range(s.length)]

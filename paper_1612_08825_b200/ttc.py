@@ -20,6 +20,7 @@ fp32 path.  run_sequence_batch() is the batched entry the benchmark uses.
 from __future__ import annotations
 
 import ctypes
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -263,11 +264,25 @@ def run_sequence_host(frames: np.ndarray, level: int | None = 0, max_level: int 
     L = _lib.load()
     nbytes = L.ct_run_sequence_host_workspace_bytes(dt, V, n, h, w, lv, ml)
     ws = _lib.workspace(nbytes, "cuda")
-    est = torch.empty((V, n - 1, 10), dtype=torch.float64).pin_memory()
+    est = _pinned_rows(V * (n - 1) * 10)
     _lib.check(L.ct_run_sequence_host(dt, ctypes.c_void_p(hptr), V, n, h, w, lv, ml, float(c_min),
                                       ctypes.c_void_p(est.data_ptr()), _lib.ptr(ws), nbytes, _lib.stream_ptr()))
     torch.cuda.current_stream().synchronize()
-    return est.numpy()
+    return est.numpy().reshape(V, n - 1, 10).copy()
+
+
+_PINNED = threading.local()
+
+
+def _pinned_rows(count: int) -> torch.Tensor:
+    """A reused page-locked staging buffer for estimate rows, one per thread
+    (grown on demand; pinning a fresh buffer per call costs more than the
+    rows' D2H).  Callers copy out before returning, so results never alias."""
+    buf = getattr(_PINNED, "buf", None)
+    if buf is None or buf.numel() < count:
+        buf = torch.empty(max(count, 1 << 16), dtype=torch.float64).pin_memory()
+        _PINNED.buf = buf
+    return buf[:count]
 
 
 def _stack_pair(pair: FramePair) -> tuple[torch.Tensor, bool]:
@@ -325,8 +340,8 @@ def run_sequence(frames, level: int | None = 0, max_level: int | None = None,
     if isinstance(f, torch.Tensor) and f.is_cuda:
         est = run_sequence_batch(f[None], level=lv, max_level=max_level, c_min=c_min)[0].cpu().numpy()
     else:
-        if isinstance(f, torch.Tensor):
-            f = f.numpy()
+        if isinstance(f, torch.Tensor):  # host tensors are coerced to float64 like numpy input (ttc.py:293)
+            f = f.to(torch.float64).numpy()
         est = run_sequence_host(np.ascontiguousarray(f)[None], level=lv, max_level=max_level, c_min=c_min)[0]
     return [estimate_from_row(r) for r in est]
 

@@ -125,3 +125,22 @@ def test_row_slab_halo_exchange_matches_unsharded(world, mode):
     for rank, out0, out in _spawn(_worker_slab, world, img, k, mode):
         got[out0:out0 + out.shape[0]] = out
     assert np.array_equal(got, ref)
+
+
+def _worker_seq_more_ranks(rank, world, port, frames, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        out = parallel.run_sequence_sharded(frames, level=0, compute=_seq_compute)
+        q.put((rank, out.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_more_ranks_than_pairs():
+    # 3 frames = 2 pairs over 3 ranks: rank 2 computes nothing but joins the gather
+    frames = O.generate(32, 32, 3, 40.0, (0.45, 0.55), 8, 0.0)
+    ref = O.run_sequence(frames, level=0)
+    assert parallel.shard_pairs(3, 3)[2].n_pairs == 0
+    for rank, out in _spawn(_worker_seq_more_ranks, 3, frames):
+        assert np.array_equal(out, ref, equal_nan=True), rank
