@@ -1058,7 +1058,7 @@ constexpr int cols_per_thread_sync() {
 // a TMA map (16-byte aligned base and row pitch), else the LDG-loader kernel runs.
 template <typename T, int BC>
 bool prep_level(MomentArgs& a, CUtensorMap& tmap, const T* frames, int64_t n_videos, int n_frames, int h, int w,
-                int border, double* partials, void* dec) {
+                int border, double* partials, void* dec, int chunk = 0) {
   constexpr int BR = band_rows<T>();
   const Plan p = make_plan<T, BC>(n_videos, n_frames, h, w);
   a = MomentArgs{};
@@ -1073,7 +1073,7 @@ bool prep_level(MomentArgs& a, CUtensorMap& tmap, const T* frames, int64_t n_vid
   a.border = border;
   a.n_ctiles = p.n_ctiles;
   a.units = p.units;
-  a.chunk = p.chunk;
+  a.chunk = chunk > 0 ? std::min(chunk, n_frames - 1) : p.chunk;
   a.tile_cols = p.tile_cols;
   a.dec = dec;
   a.dh = h / 2;
@@ -1146,7 +1146,7 @@ int launch_levels_bc(const MomentLevel* lv, int n, int64_t n_videos, int n_frame
   int64_t ctas = 0;
   for (int l = 0; l < n; ++l) {
     all_tma &= prep_level<T, BC>(m.a[l], m.tmap[l], reinterpret_cast<const T*>(lv[l].frames), n_videos, n_frames,
-                                 lv[l].h, lv[l].w, border, lv[l].partials, lv[l].dec);
+                                 lv[l].h, lv[l].w, border, lv[l].partials, lv[l].dec, lv[l].chunk);
     const int n_chunks = (n_frames - 1 + m.a[l].chunk - 1) / m.a[l].chunk;
     ctas += (int64_t)m.a[l].units * n_chunks * n_videos;
     m.cta_end[l] = ctas;

@@ -25,6 +25,7 @@ struct MomentLevel {
   int h, w;
   double* partials;
   void* dec;
+  int chunk = 0;  // pairs per CTA (0: the automatic plan; >0 e.g. one chunk per video so no frame is read twice)
 };
 constexpr int kMomentLevelsPerLaunch = 8;  // n_levels <= this
 int moments_levels_launch(int dtype, const MomentLevel* lv, int n_levels, int64_t n_videos, int n_frames, int border,
