@@ -16,12 +16,15 @@ Also reported on the same line:
   e2e          the same metric through the public host API
                (run_sequence_host on pinned numpy frames, H2D of every frame
                and D2H of every estimate inside the timed region);
-  cpu_baseline the CPU oracle port (C restatement of the reference, OpenMP
-               over pairs) on rank 0, bounded sample;
+  cpu_baseline the CPU oracle port (C restatement of the reference) as a
+               pinned process pool over videos, all host cores and one core,
+               plus the unmodified Python reference (baseline/_ref) on one
+               core and on all cores; rank 0, bounded samples;
   secondary    the other BASELINE configs (conv Gpix/s, multiscale TTC).
 
---impl reference times the CPU reference restatement (oracle/, all host
-threads) on the same workload and prints the same line with impl=reference.
+--impl reference times the CPU reference restatement (oracle/, one pinned
+worker process per host core) on the same workload and prints the same line
+with impl=reference (plus the unmodified Python reference's numbers).
 """
 
 from __future__ import annotations
@@ -168,50 +171,150 @@ def make_videos(V: int, seed0: int = 0):
     return frames
 
 
-def cpu_baseline_sample(seconds: float = 10.0, threads: int = 0):
-    """Oracle port on this host: cfg2 video repeated until ~`seconds` of CPU work
-    (threads = 0: every host thread; 1: the reference's serial setting)."""
-    import oracle
-    f = oracle.generate(W, H, NFRAMES, 100.0, (0.5, 0.5), 0, 0.0)
-    threads = threads or len(os.sched_getaffinity(0))
-    oracle.run_sequence(f[:4], level=0, nthreads=threads)  # warm
-    n_est, t0 = 0, time.perf_counter()
-    while time.perf_counter() - t0 < seconds:
-        oracle.run_sequence(f, level=0, nthreads=threads)
-        n_est += NFRAMES - 1
-    dt = time.perf_counter() - t0
-    return {"value": n_est / dt, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{n_est // (NFRAMES - 1)} x cfg2 video (64x256x256 f64) through oracle.run_sequence, "
-                      f"{dt:.1f} s wall, OpenMP over pairs"}
+# ---------------------------------------------------------------- CPU legs ---
+# The CPU baselines run as a pool of single-threaded worker processes, one per
+# host core (pinned), over independent cfg2 videos (a
+# process pool over videos; the reference is serial by design).  A step = every
+# worker processes `per_worker` videos; steps are separated by a barrier and
+# timed on the host clock, so a step lasts as long as its slowest worker.
+#   kind "port":   oracle.run_sequence (the C restatement of the reference,
+#                  oracle/convtact_oracle.c), the tier's reference arm;
+#   kind "python": the unmodified reference package (Python + numba) installed
+#                  into baseline/_ref (pip --target, git-ignored, travels to the
+#                  box), numba JIT warmed in every worker before timing.
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def _host_cpus():
+    return sorted(os.sched_getaffinity(0))
+
+
+def _cpu_worker(kind, cpu, per_worker, n_steps, barrier, q):
+    try:
+        os.sched_setaffinity(0, {cpu})
+        if kind == "python":
+            sys.path.insert(0, REF_DIR)
+            import convtact
+            f = convtact.generate(convtact.SynthConfig(width=W, height=H, frames=NFRAMES, t0=100.0, foe=(0.5, 0.5),
+                                                       seed=0)).frames
+            run = lambda: convtact.run_sequence(f, level=0)  # noqa: E731
+        else:
+            import oracle
+            f = oracle.generate(W, H, NFRAMES, 100.0, (0.5, 0.5), 0, 0.0)
+            run = lambda: oracle.run_sequence(f, level=0, nthreads=1)  # noqa: E731
+        ttc0 = run()[0]
+        ttc0 = ttc0.ttc if kind == "python" else ttc0[5]
+        assert abs(ttc0 - 97.315722253398093) <= 1e-9 * 97.3, ttc0  # SURVEY 8(c) anchor: the real computation
+        q.put(("ready", cpu))
+    except Exception as exc:  # reported by the parent, never hangs it
+        q.put(("error", repr(exc)))
+        barrier.abort()
+        return
+    barrier.wait()
+    for _ in range(n_steps):
+        for _ in range(per_worker):
+            run()
+        barrier.wait()
+
+
+def cpu_pool(kind: str, workers: int, per_worker: int, steps: int, warmup: int = 1):
+    """Run `warmup + steps` pool steps; returns per-step wall times of the timed steps."""
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    cpus = _host_cpus()[:workers]
+    barrier = ctx.Barrier(len(cpus) + 1, timeout=900)
+    q = ctx.Queue()
+    env_old = {k: os.environ.get(k) for k in ("NUMBA_CACHE_DIR", "NUMBA_NUM_THREADS", "OMP_NUM_THREADS")}
+    os.environ.update(NUMBA_CACHE_DIR=os.environ.get("NUMBA_CACHE_DIR", "/tmp/ct_numba_cache"),
+                      NUMBA_NUM_THREADS="1", OMP_NUM_THREADS="1")
+    procs = [ctx.Process(target=_cpu_worker, args=(kind, c, per_worker, warmup + steps, barrier, q), daemon=True)
+             for c in cpus]
+    try:
+        for p in procs:
+            p.start()
+        for _ in procs:
+            tag, info = q.get(timeout=900)
+            if tag == "error":
+                raise RuntimeError(f"{kind} worker failed: {info}")
+        barrier.wait()  # every worker set up (inputs built, JIT warm, anchor checked)
+        times = []
+        t = time.perf_counter()
+        for k in range(warmup + steps):
+            barrier.wait()
+            now = time.perf_counter()
+            if k >= warmup:
+                times.append(now - t)
+            t = now
+        for p in procs:
+            p.join(timeout=60)
+        return times, len(cpus)
+    finally:
+        for p in procs:
+            if p.is_alive():
+                p.kill()
+        for k, v in env_old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def cpu_measure(kind: str, workers: int, per_worker: int, steps: int, warmup: int = 1):
+    times, n = cpu_pool(kind, workers, per_worker, steps, warmup)
+    n_est = n * per_worker * (NFRAMES - 1) * steps
+    tot = sum(times)
+    what = ("C restatement of the reference (oracle/convtact_oracle.c)" if kind == "port"
+            else "unmodified reference package convtact (Python + numba, baseline/_ref)")
+    return {"value": n_est / tot, "unit": UNIT, "cores": n, "kind": "port" if kind == "port" else "reference",
+            "seconds": tot, "steps": steps, "ms_per_step": tot / steps * 1e3,
+            "sample": f"{n} pinned single-threaded worker process(es) x {per_worker} cfg2 video(s) (64x256x256 f64, "
+                      f"run_sequence level 0) per step, {steps} timed steps after {warmup} warm-up, {tot:.1f} s; "
+                      f"{what}"}
+
+
+def cpu_baselines(seconds_scale: float = 1.0):
+    """Port on all cores (the headline CPU number) and on one core, plus the
+    unmodified Python reference on one core and on all cores."""
+    ncpu = len(_host_cpus())
+    out = cpu_measure("port", ncpu, 16, max(2, int(10 * seconds_scale)))
+    out["one_core"] = cpu_measure("port", 1, 16, max(2, int(6 * seconds_scale)))
+    py = {}
+    if os.path.isdir(os.path.join(REF_DIR, "convtact")):
+        try:
+            py["one_core"] = cpu_measure("python", 1, 2, max(2, int(5 * seconds_scale)))
+            py["all_cores"] = cpu_measure("python", ncpu, 2, max(2, int(5 * seconds_scale)))
+        except Exception as exc:
+            py["error"] = repr(exc)
+    else:
+        py["unavailable"] = "baseline/_ref missing (pip install --no-index --no-deps --target baseline/_ref <reference>)"
+    out["reference_python"] = py
+    return out
 
 
 def run_reference(args, world, rank):
+    """The reference arm: the port (the tier's CPU reference implementation of
+    the path) on every host core as a pinned process pool, K timed steps of
+    `ref_videos` videos per worker after W warm-up steps; rank 0 only."""
     if rank != 0:
         return
-    import oracle
-    threads = len(os.sched_getaffinity(0))
-    f = oracle.generate(W, H, NFRAMES, 100.0, (0.5, 0.5), 0, 0.0)
-    per_step = max(1, args.ref_videos)
-    for _ in range(args.warmup):
-        oracle.run_sequence(f, level=0, nthreads=threads)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        for _ in range(per_step):
-            oracle.run_sequence(f, level=0, nthreads=threads)
-    dt = time.perf_counter() - t0
-    n = args.steps * per_step * (NFRAMES - 1)
-    value = n / dt
+    ncpu = len(_host_cpus())
+    m = cpu_measure("port", ncpu, max(1, args.ref_videos), args.steps, args.warmup)
+    py = {}
+    if os.path.isdir(os.path.join(REF_DIR, "convtact")) and not args.quick:
+        try:
+            py["one_core"] = cpu_measure("python", 1, 2, 4)
+            py["all_cores"] = cpu_measure("python", ncpu, 2, 4)
+        except Exception as exc:
+            py["error"] = repr(exc)
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+        "impl": "reference", "metric": METRIC, "value": m["value"], "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": m["ms_per_step"], "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "cfg2 single-scale TTC fp64, 64x256x256 approach video",
-                   "videos_per_step": per_step, "parallelism": f"cpu x{threads} threads (rank 0 only)"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{per_step} cfg2 video(s) per step through the C restatement of the reference "
-                                   f"(oracle/convtact_oracle.c; the reference itself is Python+numba and does not "
-                                   f"travel to the GPU box)"},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                   "videos_per_worker_per_step": m["sample"], "parallelism": f"cpu x{ncpu} processes (rank 0 only)"},
+        "cpu_baseline": {k: m[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "reference_python": py,
+        "e2e": {"value": m["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
@@ -286,37 +389,48 @@ def secondary_configs(quick: bool):
 
 def cfg5_sharded(quick: bool, world: int, rank: int):
     """BASELINE config 5, the full multiscale stream (8 videos x 1024 frames of 1080x1920 fp32,
-    max_level=3), sharded over the ranks: rank r builds and processes videos [8r/N, 8(r+1)/N) on
-    its own GPU (no data exchange; 8.5 GB of frames per video stay resident).  Timed with CUDA
-    events between barriers, max over ranks; est/s = every pair of every video / that time
-    (strong scaling: the 8-video job is fixed).  quick: 1 video x 64 frames."""
+    max_level=3), frames sharded over the ranks with a one-frame temporal halo:
+    rank r owns pairs [p0, p1) of EVERY video and builds only frames p0..p1 of each on its own
+    GPU; the step is parallel.run_sequence_sharded (the local multiscale pipeline over all
+    eight shards in one call, then one all_gather of the 80-byte estimate rows).  Timed with
+    CUDA events between barriers, max over ranks; est/s = every pair of every video / that time
+    (strong scaling: the 8-video job is fixed; any N <= 1023 is valid).  quick: 1 video x 64 frames."""
     import torch
     import paper_1612_08825_b200 as ct
+    from paper_1612_08825_b200 import parallel
     nv_total, nf = (1, 64) if quick else (8, 1024)
-    lo, hi = rank * nv_total // world, (rank + 1) * nv_total // world
-    nv = hi - lo
-    fr = None
-    if nv:
-        fr = torch.empty((nv, nf, 1080, 1920), dtype=torch.float32, device="cuda")
-        for i, v in enumerate(range(lo, hi)):
-            ct.approach_stream(nf, 1080, 1920, seed=1000 + v, dtype=torch.float32, out=fr[i])
+    me = parallel.shard_pairs(nf, world)[rank]
+    a, b = me.frames
+    fr = torch.empty((nv_total, b - a, 1080, 1920), dtype=torch.float32, device="cuda")
+    for v in range(nv_total):
+        ct.approach_stream(nf, 1080, 1920, seed=1000 + v, dtype=torch.float32, out=fr[v], frame_range=(a, b))
     st = torch.cuda.current_stream()
+    group = None
+
+    def step(**kw):
+        if kw.get("level") == 0:  # the level-0 fused kernel alone on this rank's shards
+            return ct.run_sequence_batch(fr, **kw) if me.n_pairs else None
+        return parallel.run_sequence_sharded(fr, max_level=3, frames_are_local=True, n_frames=nf, group=group)
 
     def timed(**kw):
-        if nv:
-            ct.run_sequence_batch(fr, **kw)  # warm (workspace allocation)
+        rows = step(**kw)  # warm (workspace allocation)
         torch.cuda.synchronize()
         barrier(world)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         reps = 3
         e0.record(st)
         for _ in range(reps):
-            if nv:
-                ct.run_sequence_batch(fr, **kw)
+            rows = step(**kw)
         e1.record(st)
         e1.synchronize()
-        return max_over_ranks(e0.elapsed_time(e1) / reps * 1e-3, world)
+        return max_over_ranks(e0.elapsed_time(e1) / reps * 1e-3, world), rows
 
+    t, rows = timed(max_level=3)
+    if rank == 0 and not quick:  # the sharded rows are the whole job's, in order
+        assert tuple(rows.shape) == (nv_total, nf - 1, 10), rows.shape
+    t0, _ = timed(level=0)
+    del fr
+    torch.cuda.empty_cache()
     hbm, _ = load_peaks()
     n_est = nv_total * (nf - 1)
     bytes_ = n_est * 4 * 1080 * 1920
@@ -325,14 +439,12 @@ def cfg5_sharded(quick: bool, world: int, rank: int):
         ext.append((ext[-1][0] // 2, ext[-1][1] // 2))
     pipe_bpf = 4 * (ext[0][0] * ext[0][1] + 4 * sum(hh * ww for hh, ww in ext[1:]))
     pipe_bytes = nv_total * nf * pipe_bpf
-    t = timed(max_level=3)
-    t0 = timed(level=0)
-    del fr
-    torch.cuda.empty_cache()
     return {"est_s": n_est / t, "videos": nv_total, "frames": nf, "n_gpus": world,
-            "videos_per_gpu": f"{nv_total // world}-{-(-nv_total // world)}", "ms_per_step": t * 1e3,
+            "pairs_per_gpu_per_video": f"{(nf - 1) // world}-{-(-(nf - 1) // world)}", "ms_per_step": t * 1e3,
             "input_bytes": nv_total * nf * 1080 * 1920 * 4,
-            "scaling": "strong (the 8-video job split over the ranks, no data exchange)",
+            "api": "paper_1612_08825_b200.parallel.run_sequence_sharded (frames_are_local, 4-D)",
+            "scaling": "strong (the 8-video job split by frame ranges with a one-frame halo; one all_gather of "
+                       "the estimate rows)",
             "roofline": {"bound": "hbm", "achieved": bytes_ / t / 1e9 / world, "peak": hbm, "unit": "GB/s per GPU",
                          "frac": bytes_ / t / 1e9 / world / hbm,
                          "note": "whole pipeline (level-0 moments + block means, blurs, levels 1-3, epilogue)"},
@@ -357,7 +469,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--videos", type=int, default=256, help="cfg2 videos per GPU per step")
-    ap.add_argument("--ref-videos", type=int, default=16, help="videos per step for --impl reference (enough pairs for every host thread)")
+    ap.add_argument("--ref-videos", type=int, default=16, help="videos per worker process per step for --impl reference")
     ap.add_argument("--e2e-videos", type=int, default=32)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-secondary", action="store_true")
@@ -469,6 +581,28 @@ def main():
            "h2d_bytes_per_step": Ve * NFRAMES * H * W * 8, "d2h_bytes_per_step": Ve * (NFRAMES - 1) * 10 * 8,
            "videos_per_step": Ve, "api": "paper_1612_08825_b200.run_sequence_host (ct_run_sequence_host)"}
     del host
+    # the drop-in call a reference user makes (ttc.py:282-305): run_sequence on one
+    # pageable float64 numpy video at a time, a list of TtcEstimate back
+    Vd = min(8, V)
+    vids = [frames[v].cpu().numpy() for v in range(Vd)]
+    warm = ct.run_sequence(vids[0], level=0)
+    if rank == 0:  # rank 0's video 0 is BASELINE config 2 itself
+        assert abs(warm[0].ttc - 97.315722253398093) <= 1e-9 * 97.3, warm[0]
+    torch.cuda.synchronize()
+    barrier(world)
+    d_reps = 3
+    t0 = time.perf_counter()
+    for _ in range(d_reps):
+        for vid in vids:
+            ests = ct.run_sequence(vid, level=0)
+    d_dt = max_over_ranks((time.perf_counter() - t0) / d_reps, world)
+    assert len(ests) == NFRAMES - 1
+    e2e["drop_in_run_sequence"] = {
+        "value": world * Vd * (NFRAMES - 1) / d_dt, "unit": UNIT, "videos_per_step": Vd,
+        "h2d_bytes_per_step": Vd * NFRAMES * H * W * 8, "d2h_bytes_per_step": Vd * (NFRAMES - 1) * 10 * 8,
+        "api": "paper_1612_08825_b200.run_sequence(numpy [64,256,256] float64, pageable) -> list[TtcEstimate], "
+               "one call per video (host wall clock, max over ranks)"}
+    del vids
 
     secondary = None
     if not args.no_secondary:
@@ -484,10 +618,7 @@ def main():
             c5 = {"error": repr(exc)}
         if rank == 0:
             secondary["cfg5_multiscale_fp32_1080p"] = c5
-    cpu = cpu_baseline_sample(args.cpu_seconds) if (rank == 0 and world == 1) else None
-    if cpu is not None:  # the reference is serial by design; report one core too
-        one = cpu_baseline_sample(min(3.0, args.cpu_seconds), threads=1)
-        cpu["one_core"] = {"value": one["value"], "unit": one["unit"], "cores": 1, "sample": one["sample"]}
+    cpu = cpu_baselines(args.cpu_seconds / 10.0) if (rank == 0 and world == 1) else None
 
     if rank == 0:
         line = {

@@ -694,12 +694,24 @@ __device__ __forceinline__ void moments_ws_body(const MomentArgs& a, const CUten
     // fp32 frames: per-thread epilogue and warp reduction in fp32 (the FP64
     // pipe is half rate); fp64 frames: fp64 throughout
     using E = typename std::conditional<sizeof(T) == 4, float, double>::type;
+#ifdef CT_PROBE_NO_EPI  // probing only: the per-pair epilogue and warp reduction removed (wrong sums)
+    {
+      ACC acc = 0;
+#pragma unroll
+      for (int c = 0; c < CPT; ++c)
+#pragma unroll
+        for (int q = 0; q < 10; ++q) acc += mc[c][q];
+      double* ps = part + (size_t)(i % S::NS) * NW * 10;
+      if (lane < 10) ps[wid * 10 + lane] = (double)acc;
+    }
+#else
     E o[10];
     thread_sums<ACC, CPT, E, kRaw, HR>(mc, in_col, xc, yc0, o);
     int idx;
     const double wsum = (double)warp_reduce10<E>(o, lane, idx);
     double* ps = part + (size_t)(i % S::NS) * NW * 10;
     if ((lane & 1) == 0 && idx >= 0) ps[wid * 10 + idx] = wsum;
+#endif
     // Pair i - (NB - 1) is complete: frame i + 1 (awaited above) was loaded
     // only after every warp released frame i + 1 - NB, which each warp does
     // after depositing that pair.  Its combine rotates over the warps, so no

@@ -70,6 +70,8 @@ def collective_device(group=None) -> torch.device:
 def _default_compute(frames_local, level, max_level, c_min):
     from .ttc import run_sequence_batch
     t = frames_local if isinstance(frames_local, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(frames_local))
+    if t.ndim == 4:  # a batch of videos' shards [V, frames, h, w]
+        return run_sequence_batch(t.cuda(), level=level, max_level=max_level, c_min=c_min)
     return run_sequence_batch(t.cuda()[None], level=level, max_level=max_level, c_min=c_min)[0]
 
 
@@ -79,35 +81,41 @@ def run_sequence_sharded(frames, level=0, max_level=None, c_min=1e-9, group=None
 
     ``frames`` is either the whole stack (each rank slices its shard) or, with
     frames_are_local=True, this rank's shard frames p0..p1 already (then pass
-    n_frames, the global frame count).  Every rank returns the full, ordered
-    result (gathered with one all_gather; rows identical to the 1-GPU run) on
-    collective_device(group): the GPU under NCCL, the host under gloo.
-    Ranks beyond the pair count compute nothing and still join the gather.
+    n_frames, the global frame count).  A 4-D ``frames`` [V, n, h, w] shards
+    every video the same way (one launch for all videos' shards, one
+    all_gather) and returns [V, n_frames - 1, 10].  Every rank returns the
+    full, ordered result (gathered with one all_gather; rows identical to the
+    1-GPU run) on collective_device(group): the GPU under NCCL, the host
+    under gloo.  Ranks beyond the pair count compute nothing and still join
+    the gather.
     """
     compute = compute or _default_compute
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
-    n = n_frames if frames_are_local else frames.shape[0]
+    batched = frames.ndim == 4
+    n = n_frames if frames_are_local else frames.shape[1 if batched else 0]
     if n is None:
         raise ValueError("n_frames is required with frames_are_local=True")
     plan = shard_pairs(n, world)
     me = plan[rank]
-    local = frames if frames_are_local else frames[me.frames[0]:me.frames[1]]
+    a, b = me.frames
+    local = frames if frames_are_local else (frames[:, a:b] if batched else frames[a:b])
+    lead = (frames.shape[0],) if batched else ()
     if me.n_pairs > 0:
         rows = compute(local, level, max_level, c_min)
         rows = torch.as_tensor(rows, dtype=torch.float64)
     else:  # more ranks than pairs: this rank only takes part in the gather
-        rows = torch.empty((0, 10), dtype=torch.float64)
+        rows = torch.empty(lead + (0, 10), dtype=torch.float64)
     if world == 1:
         return rows
     dev = collective_device(group)
     rows = rows.to(dev)
     width = max(s.n_pairs for s in plan)
-    buf = torch.full((width, 10), float("nan"), dtype=torch.float64, device=dev)
-    buf[:me.n_pairs] = rows
+    buf = torch.full(lead + (width, 10), float("nan"), dtype=torch.float64, device=dev)
+    buf[..., :me.n_pairs, :] = rows
     gathered = [torch.empty_like(buf) for _ in range(world)]
     dist.all_gather(gathered, buf, group=group)
-    return torch.cat([g[:s.n_pairs] for g, s in zip(gathered, plan)])
+    return torch.cat([g[..., :s.n_pairs, :] for g, s in zip(gathered, plan)], dim=-2)
 
 
 # ----------------------------------------------------------- row slabs ---

@@ -228,23 +228,32 @@ def approach_segments(frames: int, seed: int, t0_range=(50.0, 500.0), min_ttc: f
 
 
 def approach_stream(frames: int, height: int, width: int, seed: int, dtype=torch.float32,
-                    out: torch.Tensor | None = None, foe=(0.5, 0.5)) -> tuple[torch.Tensor, np.ndarray]:
+                    out: torch.Tensor | None = None, foe=(0.5, 0.5),
+                    frame_range: tuple[int, int] | None = None) -> tuple[torch.Tensor, np.ndarray]:
     """A long synthetic approach video on the device (BASELINE config 5 inputs).
 
     Returns (frames [frames, h, w] in ``dtype``, truth ttc per frame with NaN
     on the first frame of every segment after the first -- the pair ending
     there spans a cut).  Frames are generated in float64 and rounded to
-    ``dtype`` (SURVEY.md section 8(d) seeding convention).
+    ``dtype`` (SURVEY.md section 8(d) seeding convention).  frame_range=(a, b)
+    builds only frames a..b-1 of the same stream (a temporal shard: its
+    frames equal those of the whole-stream call), returned as [b - a, h, w].
     """
+    a, b = (0, frames) if frame_range is None else (int(frame_range[0]), int(frame_range[1]))
+    if not 0 <= a <= b <= frames:
+        raise ValueError(f"frame_range {frame_range} outside [0, {frames}]")
     if out is None:
-        out = torch.empty((frames, height, width), dtype=dtype, device="cuda")
-    truth = np.empty(frames)
+        out = torch.empty((b - a, height, width), dtype=dtype, device="cuda")
+    truth = np.empty(b - a)
     foe_px = (foe[0] * width, foe[1] * height)
     for s in approach_segments(frames, seed):
+        lo, hi = max(a, s.start), min(b, s.start + s.length)
+        if lo >= hi:
+            continue
         tex = make_texture_device(width, height, s.texture_seed)
-        mags = [s.t0 / (s.t0 - t) for t in range(s.length)]
-        zoom_frames(tex, foe_px, mags, dtype=dtype, out=out[s.start:s.start + s.length])
-        truth[s.start:s.start + s.length] = [s.t0 - t for t in range(s.length)]
-        if s.start > 0:
-            truth[s.start] = np.nan
+        mags = [s.t0 / (s.t0 - (t - s.start)) for t in range(lo, hi)]
+        zoom_frames(tex, foe_px, mags, dtype=dtype, out=out[lo - a:hi - a])
+        truth[lo - a:hi - a] = [s.t0 - (t - s.start) for t in range(lo, hi)]
+        if s.start > 0 and lo == s.start:
+            truth[lo - a] = np.nan
     return out, truth

@@ -20,7 +20,7 @@ def run_bench(*args, env=None):
 
 
 def test_reference_arm_json_line():
-    r = run_bench("--impl", "reference", "--steps", "1", "--warmup", "3", "--ref-videos", "1")
+    r = run_bench("--impl", "reference", "--steps", "1", "--warmup", "3", "--ref-videos", "1", "--quick")
     assert r.returncode == 0, r.stderr[-2000:]
     lines = [l for l in r.stdout.splitlines() if l.strip().startswith("{")]
     assert len(lines) == 1
@@ -31,6 +31,8 @@ def test_reference_arm_json_line():
     assert d["impl"] == "reference" and d["value"] > 0 and d["warmup"] >= 3
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+    # one pinned single-threaded worker process per host core
+    assert d["cpu_baseline"]["cores"] == len(os.sched_getaffinity(0))
 
 
 @pytest.mark.skipif(__import__("torch").cuda.is_available(), reason="checks the no-GPU failure mode")

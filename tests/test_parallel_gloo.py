@@ -144,3 +144,31 @@ def test_more_ranks_than_pairs():
     assert parallel.shard_pairs(3, 3)[2].n_pairs == 0
     for rank, out in _spawn(_worker_seq_more_ranks, 3, frames):
         assert np.array_equal(out, ref, equal_nan=True), rank
+
+
+def _seq_compute_batched(frames, level, max_level, c_min):
+    f = np.asarray(frames)
+    if f.ndim == 3:
+        return _seq_compute(f, level, max_level, c_min)
+    return torch.stack([_seq_compute(v, level, max_level, c_min) for v in f])
+
+
+def _worker_seq_batched(rank, world, port, vids, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        me = parallel.shard_pairs(vids.shape[1], world)[rank]
+        out = parallel.run_sequence_sharded(vids[:, me.frames[0]:me.frames[1]], max_level=2, frames_are_local=True,
+                                            n_frames=vids.shape[1], compute=_seq_compute_batched)
+        q.put((rank, out.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_batched_videos_sharded_by_frames():
+    # the bench's config-5 layout: every rank holds frames p0..p1 of EVERY video
+    vids = np.stack([O.generate(48, 40, 7, 30.0 + 10 * v, (0.45, 0.55), 20 + v, 0.01) for v in range(3)])
+    ref = np.stack([O.run_sequence(v, max_level=2) for v in vids])
+    for rank, out in _spawn(_worker_seq_batched, 3, vids):
+        assert out.shape == (3, 6, 10)
+        assert np.array_equal(out, ref, equal_nan=True), rank

@@ -43,6 +43,10 @@ def _worker(rank, world, port, frames, img, k, q):
         loc = torch.from_numpy(frames[me.frames[0]:me.frames[1]]).cuda()
         res["seq_local"] = parallel.run_sequence_sharded(loc, level=0, frames_are_local=True,
                                                          n_frames=frames.shape[0]).cpu().numpy()
+        # every video sharded by frames (the bench's config-5 layout), one call for all shards
+        vids = torch.from_numpy(np.stack([frames, frames[::-1].copy()])).float().cuda()
+        res["batched"] = parallel.run_sequence_sharded(vids[:, me.frames[0]:me.frames[1]], max_level=2,
+                                                       frames_are_local=True, n_frames=frames.shape[0]).cpu().numpy()
         # row slabs of one image, K-1 halo rows exchanged (CUDA ct_xcorr_nd per slab)
         m0, n0 = img.shape[0], k.shape[0]
         plan = parallel.slab_plan(m0, m0 + n0 - 1, n0 - 1, n0, world)
@@ -76,6 +80,8 @@ def test_sharded_data_plane_cuda_compute(world):
     full = ct.run_sequence_batch(torch.from_numpy(frames).cuda()[None], level=0)[0].cpu().numpy()
     full_ms = ct.run_sequence_batch(torch.from_numpy(frames.astype(np.float32)).cuda()[None],
                                     max_level=3)[0].cpu().numpy()
+    vids = torch.from_numpy(np.stack([frames, frames[::-1].copy()])).float().cuda()
+    full_b = ct.run_sequence_batch(vids, max_level=2).cpu().numpy()
     ref = O.run_sequence(frames, level=0)
     ref_conv = O.direct(img, k, "full", "zero", flip=False)
     got_conv = np.zeros_like(ref_conv)
@@ -83,8 +89,21 @@ def test_sharded_data_plane_cuda_compute(world):
         assert np.array_equal(r["seq"], full, equal_nan=True), rank
         assert np.array_equal(r["seq_local"], full, equal_nan=True), rank
         assert np.array_equal(r["ms"], full_ms, equal_nan=True), rank
+        assert np.array_equal(r["batched"], full_b, equal_nan=True), rank
         o0, out = r["slab"]
         got_conv[o0:o0 + out.shape[0]] = out
     fin = np.isfinite(ref[:, 5])
     assert np.max(np.abs(full[fin, 5] - ref[fin, 5]) / np.abs(ref[fin, 5])) <= 1e-9
     assert np.array_equal(got_conv, ref_conv)  # fp64 conv is bit-exact to the oracle
+
+
+def test_approach_stream_frame_range_is_a_shard_of_the_stream():
+    # config-5 temporal shards build only their frames; they equal the whole stream's
+    import paper_1612_08825_b200.synth as S
+    full, truth = S.approach_stream(40, 64, 96, seed=1004, dtype=torch.float32)
+    for a, b in ((0, 40), (25, 35), (31, 32), (10, 10)):
+        part, tr = S.approach_stream(40, 64, 96, seed=1004, dtype=torch.float32, frame_range=(a, b))
+        assert torch.equal(part, full[a:b])
+        assert np.array_equal(tr, truth[a:b], equal_nan=True)
+    with pytest.raises(ValueError):
+        S.approach_stream(40, 64, 96, seed=1004, frame_range=(5, 41))
