@@ -320,14 +320,45 @@ def run_reference(args, world, rank):
 
 
 DP_PER_PX = 711.539e6 * 32 / (256 * 63 * 255 * 255)  # ncu FP64 warp instructions x 32 lanes per grid pixel (21.7)
-FP64_LANE_PEAK = 32.2e12 / 2
 
 
-def secondary_configs(quick: bool):
+def fma_peaks():
+    """FP32 (FFMA) and FP64 (DFMA) TFLOP/s measured in this run by the FMA-chain
+    probe (tools/fp_peak_lib.cu, built by __graft_entry__.build()), plus the
+    theoretical peaks at the SM clock NVML reports (148 SMs x 128 / 64 lanes x 2)."""
+    import ctypes
+    import torch
+    out = {}
+    so = os.path.join(ROOT, "tools", "libfp_peak.so")
+    try:
+        lib = ctypes.CDLL(so)
+        lib.ct_probe_fma_tflops.restype = ctypes.c_double
+        lib.ct_probe_fma_tflops.argtypes = [ctypes.c_int]
+        out["fp32"] = float(lib.ct_probe_fma_tflops(0))
+        out["fp64"] = float(lib.ct_probe_fma_tflops(1))
+        out["kind"] = "measured in this run (FMA-chain probe, tools/fp_peak_lib.cu)"
+    except OSError:
+        out["fp32"], out["fp64"] = 72.2, 30.2
+        out["kind"] = "fallback: round-2 fp_peak.cu measurement on a B200 box (probe library missing)"
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        mhz = pynvml.nvmlDeviceGetClockInfo(pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device()),
+                                            pynvml.NVML_CLOCK_SM)
+    except Exception:
+        mhz = 1965
+    out["theoretical_at_clock"] = {"sm_mhz": mhz, "fp32": sms * 128 * 2 * mhz * 1e6 / 1e12,
+                                   "fp64": sms * 64 * 2 * mhz * 1e6 / 1e12}
+    return out
+
+
+def secondary_configs(quick: bool, peaks):
     """Other BASELINE configs, each timed with CUDA events (not the headline)."""
     import torch
     import paper_1612_08825_b200 as ct
     out = {}
+    p32, p64 = peaks["fp32"], peaks["fp64"]
     st = torch.cuda.current_stream()
 
     def timeit(fn, reps):
@@ -364,9 +395,9 @@ def secondary_configs(quick: bool):
     t = timeit(lambda: ct.direct_batch(s3, k3, out=o3), 5)
     fl = B3 * 2.0 * 128 ** 3 * 343
     out["cfg3_conv3d_fp32_7^3"] = {"gpix_s": B3 * 134 ** 3 / t / 1e9, "batch": B3, "ms_per_launch": t * 1e3,
-                                   "roofline": {"bound": "fp32", "achieved": fl / t / 1e12, "peak": 69.3,
-                                                "unit": "TFLOP/s", "frac": fl / t / 1e12 / 69.3,
-                                                "peak_note": "FFMA-chain microbenchmark on the box (tools/fp_peak.cu)"}}
+                                   "roofline": {"bound": "fp32", "achieved": fl / t / 1e12, "peak": p32,
+                                                "unit": "TFLOP/s", "frac": fl / t / 1e12 / p32,
+                                                "peak_note": peaks["kind"]}}
     s1, o1 = s3[:1].contiguous(), o3[:1].contiguous()
     out["cfg3_conv3d_fp32_7^3"]["single_call_ms"] = timeit(lambda: ct.direct_batch(s1, k3, out=o1), 20) * 1e3
     del s3, o3, s1, o1
@@ -378,12 +409,30 @@ def secondary_configs(quick: bool):
     t = timeit(lambda: ct.direct_batch(s4, k4, out=o4), 5)
     fl = B4 * 2.0 * 2048 ** 2 * 961
     out["cfg4_conv2d_fp32_31x31"] = {"gpix_s": B4 * 2078 ** 2 / t / 1e9, "batch": B4, "ms_per_launch": t * 1e3,
-                                     "roofline": {"bound": "fp32", "achieved": fl / t / 1e12, "peak": 69.3,
-                                                  "unit": "TFLOP/s", "frac": fl / t / 1e12 / 69.3,
-                                                  "peak_note": "FFMA-chain microbenchmark on the box (tools/fp_peak.cu)"}}
+                                     "roofline": {"bound": "fp32", "achieved": fl / t / 1e12, "peak": p32,
+                                                  "unit": "TFLOP/s", "frac": fl / t / 1e12 / p32,
+                                                  "peak_note": peaks["kind"]}}
     s1, o1 = s4[:1].contiguous(), o4[:1].contiguous()
     out["cfg4_conv2d_fp32_31x31"]["single_call_ms"] = timeit(lambda: ct.direct_batch(s1, k4, out=o1), 10) * 1e3
     del s4, o4, s1, o1
+    # widths without a tiled instantiation (the width-generic strip kernel):
+    # 13x13 fp64 (the reference's direct/FFT crossover, test_output.txt:206) on
+    # cfg1-sized images, and 33x33 fp32 on cfg4-sized images; FP-bound
+    for name, dt, shp, kw, bt, pk in (("w13_conv2d_fp64_13x13", torch.float64, (256, 256), 13, 2 if quick else 512, p64),
+                                      ("w33_conv2d_fp32_33x33", torch.float32, (2048, 2048), 33, 2, p32)):
+        sw = torch.rand((bt,) + shp, dtype=dt, device="cuda")
+        kwt = np.random.Generator(np.random.PCG64(1)).standard_normal((kw, kw))
+        if dt == torch.float32:
+            kwt = kwt.astype(np.float32)
+        ow = torch.empty((bt, shp[0] + kw - 1, shp[1] + kw - 1), dtype=dt, device="cuda")
+        t = timeit(lambda: ct.direct_batch(sw, kwt, out=ow), 5)
+        fl = bt * 2.0 * shp[0] * shp[1] * kw * kw
+        out[name] = {"gpix_s": ow.numel() / t / 1e9, "batch": bt, "ms_per_launch": t * 1e3,
+                     "kernel": "xcorr_strip (runtime width, 8-tap strips)",
+                     "roofline": {"bound": "fp64" if dt == torch.float64 else "fp32", "achieved": fl / t / 1e12,
+                                  "peak": pk, "unit": "TFLOP/s", "frac": fl / t / 1e12 / pk,
+                                  "peak_note": peaks["kind"]}}
+        del sw, ow
     return out
 
 
@@ -541,6 +590,8 @@ def main():
 
     # roofline of the dominant kernel: its CUDA-event time inside the timed region (t_k above)
     hbm, peak_kind = load_peaks()
+    peaks = fma_peaks()  # FP32 / FP64 FMA rates measured now, outside the timed region
+    fp64_lane_peak = peaks["fp64"] * 1e12 / 2
     achieved = V * (NFRAMES - 1) * BYTES_PER_EST / t_k / 1e9
     tr = load_ncu_traffic("ttc_moments_ws_kernel<double>/cfg2")
     traffic = None
@@ -556,9 +607,9 @@ def main():
             # (sweep 20 + 7/16 band-halo row + the per-pair epilogue and warp reduction)
             "fp64_pipe": {"dp_instr_per_grid_px": DP_PER_PX,
                           "achieved_lane_ops_per_s": DP_PER_PX * V * (NFRAMES - 1) * 255 * 255 / t_k,
-                          "peak_lane_ops_per_s": FP64_LANE_PEAK,
-                          "frac": DP_PER_PX * V * (NFRAMES - 1) * 255 * 255 / t_k / FP64_LANE_PEAK,
-                          "peak_note": "32.2 TFLOP/s DFMA microbenchmark on the box (tools/fp_peak.cu) = 1.61e13 lane-ops/s"},
+                          "peak_lane_ops_per_s": fp64_lane_peak,
+                          "frac": DP_PER_PX * V * (NFRAMES - 1) * 255 * 255 / t_k / fp64_lane_peak,
+                          "peak_note": peaks["kind"] + " (DFMA lane-ops/s = TFLOP/s / 2)"},
             "hbm_read_only_probe_gbs": 7500, "hbm_read_only_note": "TMA stream of the same boxes/ring/grid without compute (tools/tma_stream2.cu); above the copy peak"}
 
     # end to end through the public host API: pinned frames in, estimates out
@@ -577,7 +628,26 @@ def main():
     e_dt = max_over_ranks((time.perf_counter() - t0) / e_steps, world)
     if rank == 0:  # rank 0's video 0 is BASELINE config 2 itself
         assert abs(est_h[0, 0, 5] - 97.315722253398093) <= 1e-9 * 97.3
-    e2e = {"value": world * Ve * (NFRAMES - 1) / e_dt, "unit": UNIT,
+    # the e2e bound: pinned host->device copy bandwidth on this box (the frames dominate the step's bytes)
+    hb = host.view(-1)[: 1 << 27]  # 1 GiB of the pinned frames
+    db = torch.empty_like(hb, device="cuda")
+    db.copy_(hb, non_blocking=True)
+    torch.cuda.synchronize()
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    c0.record(st)
+    for _ in range(3):
+        db.copy_(hb, non_blocking=True)
+    c1.record(st)
+    c1.synchronize()
+    h2d_gbs = 3 * hb.numel() * 8 / (c0.elapsed_time(c1) * 1e-3) / 1e9
+    del db
+    e2e_val = world * Ve * (NFRAMES - 1) / e_dt
+    e2e = {"value": e2e_val, "unit": UNIT,
+           "pcie_roofline": {"bound": "h2d", "h2d_gbs_measured": h2d_gbs,
+                             "ceiling_est_s": world * h2d_gbs * 1e9 / (NFRAMES * H * W * 8 / (NFRAMES - 1)),
+                             "frac": e2e_val / (world * h2d_gbs * 1e9 / (NFRAMES * H * W * 8 / (NFRAMES - 1))),
+                             "note": "pinned 1 GiB cudaMemcpy H2D timed with CUDA events on this box; ceiling = "
+                                     "that bandwidth / the frame bytes per estimate"},
            "h2d_bytes_per_step": Ve * NFRAMES * H * W * 8, "d2h_bytes_per_step": Ve * (NFRAMES - 1) * 10 * 8,
            "videos_per_step": Ve, "api": "paper_1612_08825_b200.run_sequence_host (ct_run_sequence_host)"}
     del host
@@ -608,7 +678,7 @@ def main():
     if not args.no_secondary:
         if rank == 0:
             try:
-                secondary = secondary_configs(args.quick)
+                secondary = secondary_configs(args.quick, peaks)
             except Exception as exc:  # reported, never silently dropped
                 secondary = {"error": repr(exc)}
         # config 5 runs on every rank (its videos shard over the GPUs)
@@ -634,6 +704,7 @@ def main():
             "e2e": e2e,
             "cpu_baseline": cpu,
             "gpu_launches": launches,
+            "fma_peaks": peaks,
             "clocks": clk.summary(),
             "secondary": secondary,
         }

@@ -19,9 +19,12 @@
 //    the outer loop so every staged value feeds up to TZ*TY*VX FMAs; kernel
 //    taps live in the kernel-parameter constant bank (uniform operands).
 //    NW (kernel x extent) is a compile-time parameter for the widths below.
+//  * xcorr_strip<T>: ranks 1-3, any kernel width (runtime, strips of 8
+//    compile-time taps, taps staged in shared memory): the widths without a
+//    tiled instantiation.
 //  * xcorr_generic<T>: any rank <= CT_MAXDIM and any kernel width; one thread
-//    per output, odometer over taps.  Used for ranks >= 4 and widths without
-//    a tiled instantiation.
+//    per output, odometer over taps.  Used for ranks >= 4 (and kernels too
+//    large for the strip kernel's shared memory).
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -265,6 +268,188 @@ __global__ void __launch_bounds__(256) xcorr_generic(const GenArgs a) {
     }
     reinterpret_cast<T*>(a.out)[i] = acc;
   }
+}
+
+// ---------------------------------------------------------------------------
+// Width-generic register-tiled correlation (ranks 1-3, any kernel width): the
+// xcorr_tiled schedule with the kernel's x extent a runtime value.  The taps
+// are staged once per CTA into shared memory (flip applied, every kernel row
+// padded to a multiple of C), the x taps run as strips of C compile-time
+// taps (a runtime loop over full strips plus one compile-time tail strip of
+// nw % C taps, so no padded tap is ever multiplied), and per staged input row
+// a thread loads its VX + C - 1 window values of a strip once and reuses them
+// for its TY x TZ output rows.  Per output the taps are applied in row-major
+// (j0, j1, j2) order from 0.0 (strips in order), so fp64 results are
+// bit-identical to the reference loops (_loops.py:104-198).
+template <typename T, int W, int C, int VX, int TY, int TZ>
+__device__ __forceinline__ void strip_fma(const T* __restrict__ rowp, const T* __restrict__ taps_smem, int nwp,
+                                          int izr, int r, int nz, int ny, T (&acc)[TZ][TY][VX]) {
+  using V = typename VecT<T, VX>::type;
+  constexpr int CH = (VX + W - 1 + VX - 1) / VX;
+  T v[CH * VX];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    const V q = *reinterpret_cast<const V*>(rowp + c * VX);
+    const T* qp = reinterpret_cast<const T*>(&q);
+#pragma unroll
+    for (int e = 0; e < VX; ++e) v[c * VX + e] = qp[e];
+  }
+#pragma unroll
+  for (int zi = 0; zi < TZ; ++zi) {
+    const int j0 = izr - zi;
+    if (j0 < 0 || j0 >= nz) continue;
+#pragma unroll
+    for (int yi = 0; yi < TY; ++yi) {
+      const int j1 = r - yi;
+      if (j1 < 0 || j1 >= ny) continue;
+      const T* kr = taps_smem + (j0 * ny + j1) * nwp;  // uniform address: broadcast loads
+      T kv[(W + VX - 1) / VX * VX];  // 16-byte vector loads (rows are padded to kStripC taps)
+#pragma unroll
+      for (int q = 0; q < (W + VX - 1) / VX; ++q) {
+        const V t = *reinterpret_cast<const V*>(kr + q * VX);
+        const T* tp = reinterpret_cast<const T*>(&t);
+#pragma unroll
+        for (int e = 0; e < VX; ++e) kv[q * VX + e] = tp[e];
+      }
+#pragma unroll
+      for (int j2 = 0; j2 < W; ++j2)
+#pragma unroll
+        for (int rr = 0; rr < VX; ++rr) acc[zi][yi][rr] = fmadd(kv[j2], v[rr + j2], acc[zi][yi][rr]);
+    }
+  }
+}
+
+template <typename T, int C, int VX, int TY, int TZ>
+__global__ void __launch_bounds__(256) xcorr_strip(const TileArgs a, const T* __restrict__ k, int nw, int flip) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int nwp = (nw + C - 1) / C * C;  // padded taps per kernel row
+  const int nrow_k = a.nz * a.ny;
+  T* taps_smem = reinterpret_cast<T*>(smem_raw);
+  T* tile = taps_smem + ((size_t)nrow_k * nwp + 3) / 4 * 4;  // 16-byte aligned after the taps
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  const int64_t kt = (int64_t)nrow_k * nw;
+  for (int idx = tid; idx < nrow_k * nwp; idx += nthr) {
+    const int row = idx / nwp, j2 = idx - row * nwp;
+    const int64_t t = (int64_t)row * nw + j2;
+    taps_smem[idx] = j2 < nw ? __ldg(k + (flip ? kt - 1 - t : t)) : T(0);  // padding is never multiplied
+  }
+  const int tx = tid % a.txn, ty = tid / a.txn;
+  const int BX = a.txn * VX, BY = a.tyn * TY;
+  const int x0 = blockIdx.x * BX, y0 = blockIdx.y * BY;
+  const int ny = a.ny, nz = a.nz;
+  const int64_t plane = (int64_t)a.my * a.mx;
+  const int64_t n_ztiles = a.batch * a.tiles_z;
+  const int full = nw / C, tail = nw - full * C;
+
+  for (int64_t bz = blockIdx.z; bz < n_ztiles; bz += gridDim.z) {
+    const int64_t b = bz / a.tiles_z;
+    const int z0 = (int)(bz % a.tiles_z) * TZ;
+    const T* s = reinterpret_cast<const T*>(a.s) + b * (int64_t)a.mz * plane;
+    T acc[TZ][TY][VX];
+#pragma unroll
+    for (int i = 0; i < TZ; ++i)
+#pragma unroll
+      for (int j = 0; j < TY; ++j)
+#pragma unroll
+        for (int r = 0; r < VX; ++r) acc[i][j][r] = T(0);
+    const int nzin = TZ + nz - 1;
+    for (int izr = 0; izr < nzin; ++izr) {
+      int gz = z0 - a.pz + izr;
+      if (gz < 0 || gz >= a.mz) {
+        if (a.boundary == CT_ZERO) continue;  // all-zero slice: adds nothing
+        gz = gz < 0 ? 0 : a.mz - 1;
+      }
+      __syncthreads();  // previous slice consumed (and the taps staged, first time)
+      {
+        const T* sp = s + gz * plane;
+        const int iy0 = y0 - a.py, ix0 = x0 - a.px;
+        const int total = a.sx * a.sy;
+        for (int idx = tid; idx < total; idx += nthr) {
+          const int r = idx / a.sx, c = idx - r * a.sx;
+          int gy = iy0 + r, gx = ix0 + c;
+          T v = T(0);
+          const bool in = (unsigned)gy < (unsigned)a.my && (unsigned)gx < (unsigned)a.mx;
+          if (in) {
+            v = __ldg(sp + (int64_t)gy * a.mx + gx);
+          } else if (a.boundary == CT_REPLICATE) {
+            gy = min(max(gy, 0), a.my - 1);
+            gx = min(max(gx, 0), a.mx - 1);
+            v = __ldg(sp + (int64_t)gy * a.mx + gx);
+          }
+          tile[idx] = v;
+        }
+      }
+      __syncthreads();
+      const int nrows = TY + ny - 1;
+      for (int r = 0; r < nrows; ++r) {
+        const T* rowp = tile + (ty * TY + r) * a.sx + tx * VX;
+        for (int st = 0; st < full; ++st)
+          strip_fma<T, C, C, VX, TY, TZ>(rowp + st * C, taps_smem + st * C, nwp, izr, r, nz, ny, acc);
+        const T* rt = rowp + full * C;
+        const T* kt_ = taps_smem + full * C;
+        switch (tail) {  // compile-time tail strip
+#define CT_TAIL(Wt) case Wt: strip_fma<T, Wt, C, VX, TY, TZ>(rt, kt_, nwp, izr, r, nz, ny, acc); break;
+          CT_TAIL(1) CT_TAIL(2) CT_TAIL(3) CT_TAIL(4) CT_TAIL(5) CT_TAIL(6) CT_TAIL(7)
+#undef CT_TAIL
+          default: break;
+        }
+      }
+    }
+    T* out = reinterpret_cast<T*>(a.out) + b * (int64_t)a.oz * a.oy * a.ox;
+#pragma unroll
+    for (int zi = 0; zi < TZ; ++zi) {
+      const int z = z0 + zi;
+      if (z >= a.oz) break;
+#pragma unroll
+      for (int yi = 0; yi < TY; ++yi) {
+        const int y = y0 + ty * TY + yi;
+        if (y >= a.oy) break;
+        T* orow = out + ((int64_t)z * a.oy + y) * a.ox;
+        const int x = x0 + tx * VX;
+#pragma unroll
+        for (int rr = 0; rr < VX; ++rr)
+          if (x + rr < a.ox) orow[x + rr] = acc[zi][yi][rr];
+      }
+    }
+  }
+}
+
+#ifndef CT_STRIP_TY64
+#define CT_STRIP_TY64 4
+#endif
+constexpr int kStripC = 8;  // compile-time taps per strip (a multiple of both vector widths)
+
+// smem bytes of xcorr_strip for these extents (0: does not fit one CTA)
+template <typename T>
+size_t strip_smem(const TileArgs& a, int nw, int txn, int tyn, int TY) {
+  constexpr int VX = 16 / sizeof(T);
+  const int nwp = (nw + kStripC - 1) / kStripC * kStripC;
+  const size_t taps = ((size_t)a.nz * a.ny * nwp + 3) / 4 * 4;
+  const int BX = txn * VX, BY = tyn * TY;
+  const int sx = BX - VX + (VX + nwp - 1 + VX - 1) / VX * VX;  // every strip's window loads stay in the row
+  const size_t tile = (size_t)sx * (BY + a.ny - 1);
+  const size_t bytes = (taps + tile) * sizeof(T);
+  return bytes <= 200 * 1024 ? bytes : 0;
+}
+
+template <typename T, int TY, int TZ>
+int launch_strip(const TileArgs& a0, const T* k_dev, int nw, int flip, cudaStream_t st) {
+  constexpr int VX = 16 / sizeof(T);
+  TileArgs a = a0;
+  a.txn = 32;
+  a.tyn = 8;
+  const size_t smem = strip_smem<T>(a, nw, a.txn, a.tyn, TY);
+  CT_REQUIRE(smem > 0, "kernel too large for the strip kernel");
+  const int nwp = (nw + kStripC - 1) / kStripC * kStripC;
+  a.sx = a.txn * VX - VX + (VX + nwp - 1 + VX - 1) / VX * VX;
+  a.sy = a.tyn * TY + a.ny - 1;
+  a.tiles_z = TZ > 1 ? (int)cdiv(a.oz, TZ) : a.oz;
+  auto kern = xcorr_strip<T, kStripC, VX, TY, TZ>;
+  CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 grid((unsigned)cdiv(a.ox, a.txn * VX), (unsigned)cdiv(a.oy, a.tyn * TY),
+            (unsigned)std::min<int64_t>(a.batch * a.tiles_z, 65535));
+  kern<<<grid, a.txn * a.tyn, smem, st>>>(a, k_dev, nw, flip);
+  return check_launch("xcorr_strip");
 }
 
 // ---------------------------------------------------------------------------
@@ -1742,6 +1927,45 @@ int dispatch(int ndim, const void* s, const int64_t* ms, int64_t batch, const vo
                         (k_host || cap == cudaStreamCaptureStatusNone) &&
                         (nw == 1 || nw == 2 || nw == 3 || nw == 4 || nw == 5 || nw == 6 ||
                          nw == 7 || nw == 8 || nw == 9 || nw == 11 || nw == 15 || nw == 31);
+  // shapes as 3-D (z, y, x)
+  auto as3d = [&](TileArgs& a) -> int {
+    int64_t m3[3] = {1, 1, 1}, n3[3] = {1, 1, 1}, p3[3] = {0, 0, 0}, o3[3] = {1, 1, 1};
+    for (int d = 0; d < ndim; ++d) {
+      m3[3 - ndim + d] = ms[d];
+      n3[3 - ndim + d] = ns[d];
+      p3[3 - ndim + d] = pl[d];
+      o3[3 - ndim + d] = os[d];
+    }
+    for (int d = 0; d < 3; ++d)
+      CT_REQUIRE(m3[d] < (1 << 30) && o3[d] < (1 << 30) && p3[d] < (1 << 30), "extent too large");
+    a = TileArgs{};
+    a.s = s;
+    a.out = out;
+    a.batch = batch;
+    a.mz = (int)m3[0]; a.my = (int)m3[1]; a.mx = (int)m3[2];
+    a.oz = (int)o3[0]; a.oy = (int)o3[1]; a.ox = (int)o3[2];
+    a.nz = (int)n3[0]; a.ny = (int)n3[1];
+    a.pz = (int)p3[0]; a.py = (int)p3[1]; a.px = (int)p3[2];
+    a.boundary = boundary;
+    a.tiles_z = 1;
+    return CT_OK;
+  };
+  // any other width (ranks 1-3): the width-generic strip kernel, taps read
+  // from the device kernel (no host copy, capture-safe)
+  static const bool no_strip = getenv("CT_CONV_NOSTRIP") != nullptr;  // tests: force the generic kernel
+  if (!tiled_ok && ndim <= 3 && s_elems > 0 && !no_strip) {
+    TileArgs a;
+    int rc = as3d(a);
+    if (rc) return rc;
+    const bool is3d = a.oz > 1 || a.nz > 1;
+    // rows per thread: fp64 reuses each window load over 8 output rows (the
+    // DFMA:load ratio), fp32 over 4
+    constexpr int STY = sizeof(T) == 8 ? CT_STRIP_TY64 : 4;
+    if (strip_smem<T>(a, nw, 32, 8, STY) > 0) {
+      if (is3d) return launch_strip<T, STY, 2>(a, reinterpret_cast<const T*>(k), nw, flip, st);
+      return launch_strip<T, STY, 1>(a, reinterpret_cast<const T*>(k), nw, flip, st);
+    }
+  }
   if (tiled_ok) {
     // shapes as 3-D (z, y, x)
     int64_t m3[3] = {1, 1, 1}, n3[3] = {1, 1, 1}, p3[3] = {0, 0, 0}, o3[3] = {1, 1, 1};

@@ -268,3 +268,50 @@ def test_cuda_graph_capture_replays_bit_identical():
     g.replay()
     torch.cuda.synchronize()
     assert torch.equal(out, eager)
+
+
+# widths without a tiled instantiation take the width-generic strip kernel
+# (xcorr_strip: runtime width, 8-tap compile-time strips + exact tail);
+# fp64 stays bit-identical to the reference order, fp32 within 1e-5
+STRIP_CASES = [
+    ((300,), (13,)), ((257,), (40,)), ((70, 90), (13, 13)), ((64, 77), (5, 10)), ((50, 61), (3, 16)),
+    ((41, 45), (12, 17)), ((33, 40), (20, 33)), ((19, 23, 29), (3, 4, 13)), ((12, 14, 20), (5, 2, 10)),
+]
+
+
+@pytest.mark.parametrize("ss,ks", STRIP_CASES)
+def test_width_generic_strip_kernel_fp64_bit_exact(ss, ks):
+    rng = np.random.default_rng(sum(ss) + 7 * sum(ks))
+    s = rng.random(ss)
+    k = rng.standard_normal(ks)
+    for shape in SHAPES:
+        if shape == V and any(a < b for a, b in zip(ss, ks)):
+            continue
+        for bd in BOUNDS:
+            for fn, flip in ((ct.conv_direct, True), (ct.xcorr_direct, False)):
+                got = fn(s, k, shape, bd)
+                ref = O.direct(s, k, shape.name.lower(), bd.name.lower() if shape == S else "zero", flip=flip)
+                assert np.array_equal(got, ref), (ss, ks, shape, bd, flip, np.abs(got - ref).max())
+
+
+@pytest.mark.parametrize("ss,ks", STRIP_CASES[2:7])
+def test_width_generic_strip_kernel_fp32(ss, ks):
+    rng = np.random.default_rng(3 + sum(ss))
+    s = rng.random(ss).astype(np.float32)
+    k = rng.standard_normal(ks).astype(np.float32)
+    got = ct.conv_direct(torch.from_numpy(s).cuda(), torch.from_numpy(k), F).cpu().numpy()
+    assert got.dtype == np.float32
+    assert rel_inf(got, O.direct(s.astype(np.float64), k.astype(np.float64), "full")) <= 1e-5
+
+
+def test_width_generic_batches_and_large_kernels():
+    # batched launch == the oracle per image; a 90x90 kernel (8100 taps) still stages in shared memory
+    rng = np.random.default_rng(13)
+    s = torch.from_numpy(rng.random((5, 96, 130))).cuda()
+    k = rng.standard_normal((13, 13))
+    a = ct.direct_batch(s, k, F, flip=True).cpu().numpy()
+    for i in range(5):
+        assert np.array_equal(a[i], O.direct(s[i].cpu().numpy(), k, "full"))
+    big = rng.standard_normal((90, 90))           # 8100 taps: shared-memory bound still fits
+    t = rng.random((120, 130))
+    assert np.array_equal(ct.xcorr_direct(t, big, F), O.direct(t, big, "full", flip=False))

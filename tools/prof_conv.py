@@ -16,6 +16,16 @@ elif cfg == 'cfg3':
     k = np.random.Generator(np.random.PCG64(1)).standard_normal((7, 7, 7)).astype(np.float32)
     o = torch.empty((8, 134, 134, 134), dtype=torch.float32, device='cuda')
     work = 8 * 134 ** 3
+elif cfg == 'w13':  # reference crossover width, fp64, cfg1-sized images
+    s = torch.rand((512, 256, 256), dtype=torch.float64, device='cuda')
+    k = np.random.Generator(np.random.PCG64(1)).standard_normal((13, 13))
+    o = torch.empty((512, 268, 268), dtype=torch.float64, device='cuda')
+    work = 512 * 268 * 268
+elif cfg == 'w33':  # a width past the tiled instantiations, fp32, cfg4-sized images
+    s = torch.rand((2, 2048, 2048), dtype=torch.float32, device='cuda')
+    k = np.random.Generator(np.random.PCG64(1)).standard_normal((33, 33)).astype(np.float32)
+    o = torch.empty((2, 2080, 2080), dtype=torch.float32, device='cuda')
+    work = 2 * 2080 ** 2
 else:
     s = torch.rand((2, 2048, 2048), dtype=torch.float32, device='cuda')
     k = np.random.Generator(np.random.PCG64(1)).standard_normal((31, 31)).astype(np.float32)
@@ -30,4 +40,5 @@ for _ in range(reps):
     ct.direct_batch(s, k, out=o)
 e1.record(); e1.synchronize()
 t = e0.elapsed_time(e1) / reps
-print(cfg, 'ms', t, 'Gpix/s', work / t / 1e6)
+flops = {'w13': 512 * 256 * 256 * 169 * 2, 'w33': 2 * 2048 ** 2 * 33 * 33 * 2}.get(cfg)
+print(cfg, 'ms', t, 'Gpix/s', work / t / 1e6, '' if flops is None else f'TFLOP/s {flops / t / 1e9:.2f}')

@@ -22,6 +22,11 @@ K1 = 31
 OY = 2078
 Kd = K1 * (BX + K1 - 1)
 torch.backends.cuda.matmul.allow_tf32 = True
+try:  # torch >= 2.9 spelling
+    torch.backends.cuda.matmul.fp32_precision = "tf32"
+except Exception:
+    pass
+torch.set_float32_matmul_precision("high")
 a = torch.rand((OY, Kd), device="cuda")
 b = torch.rand((Kd, BX * 16), device="cuda")  # 16 column tiles side by side: N = 16 * BX
 for _ in range(3):
@@ -36,6 +41,16 @@ e1.record()
 e1.synchronize()
 t = e0.elapsed_time(e1) / reps * 1e-3
 gemm_tf = 2.0 * OY * Kd * b.shape[1] / t / 1e12
+ab, bb = a.bfloat16(), b.bfloat16()
+for _ in range(3):
+    cb = ab @ bb
+torch.cuda.synchronize()
+e0.record()
+for _ in range(reps):
+    cb = ab @ bb
+e1.record()
+e1.synchronize()
+bf16_tf = 2.0 * OY * Kd * b.shape[1] / (e0.elapsed_time(e1) / reps * 1e-3) / 1e12
 density = K1 * K1 / Kd
 
 
@@ -52,15 +67,17 @@ def toeplitz_conv(s, k, split):
         rows = sp[j0:j0 + o0]                      # [o0, padded cols]
         win = rows[:, idx]                          # [o0, n1, o1]: win[y, j1, x] = s_pad[y + j0, x + j1]
         kk = k[j0][None, :, None]
+        def tf32(x):  # the tensor core's TF32 operand rounding (10-bit mantissa, truncation)
+            return (x.contiguous().view(torch.int32) & ~0x1FFF).view(torch.float32)
+        # products of TF32 operands are exact in fp64; accumulate in fp64 to isolate the operand rounding
         if split == 1:
-            out += torch.einsum("yjx,j->yx", win, k[j0])
+            out += torch.einsum("yjx,j->yx", tf32(win).double(), tf32(k[j0]).double()).float()
         else:
-            def tf32(x):
-                return (x.view(torch.int32) & ~0x1FFF).view(torch.float32)
             wh, kh = tf32(win), tf32(k[j0])
-            wl, kl = win - wh, k[j0] - kh
-            out += torch.einsum("yjx,j->yx", wh, kh) + (torch.einsum("yjx,j->yx", wl, kh) +
-                                                       torch.einsum("yjx,j->yx", wh, kl))
+            wl, kl = tf32(win - wh), tf32(k[j0] - kh)
+            out += (torch.einsum("yjx,j->yx", wh.double(), kh.double()) +
+                    torch.einsum("yjx,j->yx", wl.double(), kh.double()) +
+                    torch.einsum("yjx,j->yx", wh.double(), kl.double())).float()
         del kk
     return out
 
@@ -75,5 +92,5 @@ res = {}
 for split in (1, 3):
     got = toeplitz_conv(torch.from_numpy(s).cuda(), torch.from_numpy(k).cuda(), split).double().cpu().numpy()
     res[f"{split}xTF32_rel_inf"] = float(np.max(np.abs(got - ref)) / np.max(np.abs(ref)))
-print(json.dumps({"BX": BX, "gemm_shape": [OY, Kd, b.shape[1]], "tf32_gemm_tflops": gemm_tf, "density": density,
+print(json.dumps({"BX": BX, "gemm_shape": [OY, Kd, b.shape[1]], "tf32_gemm_tflops": gemm_tf, "bf16_gemm_tflops_same_shape": bf16_tf, "density": density,
                   "useful_tflops_1xtf32": gemm_tf * density, "useful_tflops_3xtf32": gemm_tf * density / 3, **res}))
