@@ -510,3 +510,21 @@ def test_synth_drop_in_helpers(tmp_path):
         f"{int(r[0])},{float(r[1])!r},{float(r[2])!r},{float(r[3])!r}\n" for r in seq.truth))
     rep = ct.score_mse(tmp_path / "pred.csv", tmp_path / "truth.csv")
     assert rep.compared + rep.excluded == 4 and rep.mse >= 0
+
+
+def test_host_paths_pageable_and_pinned_match_device():
+    """run_sequence_host streams pinned frames directly and pageable frames
+    through its pinned staging ring in 8 MB chunks (one-frame halo between
+    chunks); both equal the device-resident run bit for bit, multiscale too."""
+    g = torch.Generator(device="cuda").manual_seed(5)
+    dev = torch.rand((2, 100, 256, 256), dtype=torch.float64, device="cuda", generator=g)  # 50 MB per video
+    for kw in ({"level": 0}, {"max_level": 2}):
+        ref = ct.run_sequence_batch(dev, **kw).cpu().numpy()
+        pageable = dev.cpu().numpy()
+        pinned = dev.cpu().pin_memory()
+        assert np.array_equal(ct.run_sequence_host(pageable, **kw), ref, equal_nan=True)
+        assert np.array_equal(ct.run_sequence_host(pinned, **kw), ref, equal_nan=True)
+    f32 = dev[0].float().cpu().numpy()  # the reference-style call on a float32 array: coerced to float64
+    est = ct.run_sequence(f32, level=0)
+    want = ct.run_sequence_batch(torch.from_numpy(f32.astype(np.float64)).cuda()[None], level=0)[0].cpu().numpy()
+    assert np.array_equal(rows(est)[:, :8], want[:, :8], equal_nan=True)
