@@ -89,7 +89,6 @@ template <typename T, int BR, int NT, int BC>
 __device__ __forceinline__ void write_dec(const MomentArgs& a, const T* buf, int64_t v, int f, int gy0, int cx0,
                                           int tid) {
   constexpr int DC = BC / 2;  // dec columns per tile (at most)
-  static_assert(NT % DC == 0, "write_dec maps DC dec columns per thread row");
   const int dy0 = gy0 >> 1, dx0 = cx0 >> 1;
   const int ndy = min(BR / 2, a.dh - dy0);
   const int ndx = min((a.tile_cols + 1) >> 1, a.dw - dx0);
@@ -116,20 +115,25 @@ __device__ __forceinline__ void write_dec(const MomentArgs& a, const T* buf, int
       return;
     }
   }
-  const int xx = tid % DC;  // dec column of this thread
-  if (ndy <= 0 || xx >= ndx) return;
-  T* dst = reinterpret_cast<T*>(a.dec) + ((v * a.n_frames + f) * (int64_t)a.dh + dy0) * a.dw + dx0 + xx;
-#pragma unroll 4
-  for (int yy = tid / DC; yy < ndy; yy += NT / DC) {
+  auto mean = [&](int yy, int xx) {
     const T* p0 = buf + (2 * yy) * BC + 2 * xx;
     const T* p1 = p0 + BC;
-    T d;
-    if constexpr (sizeof(T) == 8) {
-      d = __dmul_rn(0.25, __dadd_rn(__dadd_rn(__dadd_rn(p0[0], p0[1]), p1[0]), p1[1]));
-    } else {
-      d = __fmul_rn(0.25f, __fadd_rn(__fadd_rn(__fadd_rn(p0[0], p0[1]), p1[0]), p1[1]));
+    if constexpr (sizeof(T) == 8)
+      return __dmul_rn(0.25, __dadd_rn(__dadd_rn(__dadd_rn(p0[0], p0[1]), p1[0]), p1[1]));
+    else
+      return __fmul_rn(0.25f, __fadd_rn(__fadd_rn(__fadd_rn(p0[0], p0[1]), p1[0]), p1[1]));
+  };
+  T* base = reinterpret_cast<T*>(a.dec) + ((v * a.n_frames + f) * (int64_t)a.dh + dy0) * a.dw + dx0;
+  if constexpr (NT % DC == 0) {  // a thread keeps one dec column
+    const int xx = tid % DC;
+    if (ndy <= 0 || xx >= ndx) return;
+#pragma unroll 4
+    for (int yy = tid / DC; yy < ndy; yy += NT / DC) base[(int64_t)yy * a.dw + xx] = mean(yy, xx);
+  } else {  // fewer threads than dec columns (four columns per thread)
+    for (int idx = tid; idx < ndy * DC; idx += NT) {
+      const int yy = idx / DC, xx = idx - yy * DC;
+      if (xx < ndx) base[(int64_t)yy * a.dw + xx] = mean(yy, xx);
     }
-    dst[(int64_t)yy * a.dw] = d;
   }
 }
 
@@ -376,6 +380,84 @@ __device__ __forceinline__ void sweep_c2(const float* __restrict__ A, const floa
     m[c][7] = fmaf(K, L(s3), -L(q3));
     m[c][8] = fmaf(K, L(s5), -L(q5));
     m[c][9] = fmaf(K * K, L(s3), fmaf(-(2 * K + 1), L(q3), 2 * L(qq3)));
+  }
+}
+
+// fp32 four-column sweep (CT_MOM_FOUR_COL_F32): a thread owns grid columns
+// col..col+3 as two packed f32x2 column pairs; per frame row one 16-byte load
+// gives F[col..col+3] and a 4-byte load F[col+4] (a quarter of the loads per
+// pixel of one column per thread), the shifted pairs (x+1, x+2), (x+3, x+4)
+// are assembled with moves, and the per-pair epilogue and warp reduction are
+// paid once per four columns.  Per-lane operation order is sweep()'s.
+template <int BR, bool CHECK, int BC>
+__device__ __forceinline__ void sweep_c4(const float* __restrict__ A, const float* __restrict__ B, int col, int r_beg,
+                                         int r_end, float (&m)[4][10]) {
+  float2 s1[2], s2[2], s3[2], s4[2], s5[2], s6[2], q2[2], q3[2], q5[2], qq3[2], hP[2], dP[2], sD[2];
+#pragma unroll
+  for (int p = 0; p < 2; ++p) {
+    s1[p] = s2[p] = s3[p] = s4[p] = s5[p] = s6[p] = make_float2(0.f, 0.f);
+    q2[p] = q3[p] = q5[p] = qq3[p] = make_float2(0.f, 0.f);
+  }
+  auto row = [&](int r, float2 (&nhP)[2], float2 (&ndP)[2], float2 (&nsD)[2]) {
+    const float4 a = *reinterpret_cast<const float4*>(A + r * BC + col);
+    const float4 b = *reinterpret_cast<const float4*>(B + r * BC + col);
+    const float a4 = A[r * BC + col + 4], b4 = B[r * BC + col + 4];
+    const float2 P01 = f2add(make_float2(a.x, a.y), make_float2(b.x, b.y));
+    const float2 P23 = f2add(make_float2(a.z, a.w), make_float2(b.z, b.w));
+    const float2 D01 = f2sub(make_float2(b.x, b.y), make_float2(a.x, a.y));
+    const float2 D23 = f2sub(make_float2(b.z, b.w), make_float2(a.z, a.w));
+    const float2 P12 = make_float2(P01.y, P23.x), P34 = make_float2(P23.y, a4 + b4);
+    const float2 D12 = make_float2(D01.y, D23.x), D34 = make_float2(D23.y, b4 - a4);
+    nhP[0] = f2add(P01, P12);
+    ndP[0] = f2sub(P12, P01);
+    nsD[0] = f2add(D01, D12);
+    nhP[1] = f2add(P23, P34);
+    ndP[1] = f2sub(P34, P23);
+    nsD[1] = f2add(D23, D34);
+  };
+  row(0, hP, dP, sD);
+#pragma unroll
+  for (int r = 1; r <= BR; ++r) {
+    float2 nhP[2], ndP[2], nsD[2];
+    row(r, nhP, ndP, nsD);
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      if (!CHECK || (r >= r_beg && r <= r_end)) {
+        const float2 ex = f2add(dP[p], ndP[p]), ey = f2sub(nhP[p], hP[p]), et = f2add(sD[p], nsD[p]);
+        s1[p] = f2fma(ex, ex, s1[p]);
+        s2[p] = f2fma(ex, ey, s2[p]);
+        s3[p] = f2fma(ey, ey, s3[p]);
+        s4[p] = f2fma(ex, et, s4[p]);
+        s5[p] = f2fma(ey, et, s5[p]);
+        s6[p] = f2fma(et, et, s6[p]);
+      }
+      if (r == 1) {
+        q2[p] = s2[p];
+        q3[p] = s3[p];
+        q5[p] = s5[p];
+        qq3[p] = s3[p];
+      } else {
+        q2[p] = f2add(q2[p], s2[p]);
+        q3[p] = f2add(q3[p], s3[p]);
+        q5[p] = f2add(q5[p], s5[p]);
+        qq3[p] = f2add(qq3[p], q3[p]);
+      }
+      hP[p] = nhP[p];
+      dP[p] = ndP[p];
+      sD[p] = nsD[p];
+    }
+  }
+  constexpr float K = float(BR);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int p = c >> 1;
+    auto L = [&](float2 v) { return (c & 1) ? v.y : v.x; };
+    m[c][0] = L(s1[p]); m[c][1] = L(s2[p]); m[c][2] = L(s3[p]);
+    m[c][3] = L(s4[p]); m[c][4] = L(s5[p]); m[c][5] = L(s6[p]);
+    m[c][6] = fmaf(K, L(s2[p]), -L(q2[p]));
+    m[c][7] = fmaf(K, L(s3[p]), -L(q3[p]));
+    m[c][8] = fmaf(K, L(s5[p]), -L(q5[p]));
+    m[c][9] = fmaf(K * K, L(s3[p]), fmaf(-(2 * K + 1), L(q3[p]), 2 * L(qq3[p])));
   }
 }
 
@@ -673,6 +755,13 @@ __device__ __forceinline__ void moments_ws_body(const MomentArgs& a, const CUten
       else
         sweep_c2d<HR, true, BC>(reinterpret_cast<const double*>(Ar), reinterpret_cast<const double*>(Br), col, r_beg,
                                 r_end, mc);
+    } else if constexpr (CPT == 4) {
+      if (r_beg <= 1 && r_end >= HR)
+        sweep_c4<HR, false, BC>(reinterpret_cast<const float*>(Ar), reinterpret_cast<const float*>(Br), col, 1, HR,
+                                mc);
+      else
+        sweep_c4<HR, true, BC>(reinterpret_cast<const float*>(Ar), reinterpret_cast<const float*>(Br), col, r_beg,
+                               r_end, mc);
     } else if constexpr (CPT == 2) {
       if (r_beg <= 1 && r_end >= HR)
         sweep_c2<HR, false, BC>(reinterpret_cast<const float*>(Ar), reinterpret_cast<const float*>(Br), col, 1, HR,
@@ -1056,14 +1145,20 @@ size_t ws_bytes(int64_t n_videos, int n_frames, int h, int w) {
 #ifndef CT_MOM_TWO_COL_F64
 #define CT_MOM_TWO_COL_F64 0
 #endif
+#ifndef CT_MOM_FOUR_COL_F32
+#define CT_MOM_FOUR_COL_F32 0
+#endif
 template <typename T, int BC>
 constexpr int cols_per_thread() {
-  return (sizeof(T) == 4 && kTwoColF32 && BC == 256) ? 2 : (sizeof(T) == 8 && CT_MOM_TWO_COL_F64 && BC == 256) ? 2 : 1;
+  return (sizeof(T) == 4 && CT_MOM_FOUR_COL_F32 && BC == 256) ? 4
+         : (sizeof(T) == 4 && kTwoColF32 && BC == 256)           ? 2
+         : (sizeof(T) == 8 && CT_MOM_TWO_COL_F64 && BC == 256)   ? 2
+                                                                 : 1;
 }
 // the CTA-barrier kernel (plain-load fallback) runs fp64 one column per thread
 template <typename T, int BC>
 constexpr int cols_per_thread_sync() {
-  return sizeof(T) == 8 ? 1 : cols_per_thread<T, BC>();
+  return sizeof(T) == 8 ? 1 : (cols_per_thread<T, BC>() > 2 ? 2 : cols_per_thread<T, BC>());
 }
 
 // Kernel arguments and TMA map of one level; returns whether the frames admit
