@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(256) xcorr_generic(const GenArgs a) {
 // (j0, j1, j2) order from 0.0 (strips in order), so fp64 results are
 // bit-identical to the reference loops (_loops.py:104-198).
 template <typename T, int W, int C, int VX, int TY, int TZ>
-__device__ __forceinline__ void strip_fma(const T* __restrict__ rowp, const T* __restrict__ taps_smem, int nwp,
+__device__ __forceinline__ void strip_fma(const T* __restrict__ rowp, const T* __restrict__ taps, int nwp,
                                           int izr, int r, int nz, int ny, T (&acc)[TZ][TY][VX]) {
   using V = typename VecT<T, VX>::type;
   constexpr int CH = (VX + W - 1 + VX - 1) / VX;
@@ -302,7 +302,7 @@ __device__ __forceinline__ void strip_fma(const T* __restrict__ rowp, const T* _
     for (int yi = 0; yi < TY; ++yi) {
       const int j1 = r - yi;
       if (j1 < 0 || j1 >= ny) continue;
-      const T* kr = taps_smem + (j0 * ny + j1) * nwp;  // uniform address: broadcast loads
+      const T* kr = taps + (j0 * ny + j1) * nwp;  // uniform address: constant-bank or broadcast loads
       T kv[(W + VX - 1) / VX * VX];  // 16-byte vector loads (rows are padded to kStripC taps)
 #pragma unroll
       for (int q = 0; q < (W + VX - 1) / VX; ++q) {
@@ -319,19 +319,28 @@ __device__ __forceinline__ void strip_fma(const T* __restrict__ rowp, const T* _
   }
 }
 
-template <typename T, int C, int VX, int TY, int TZ>
-__global__ void __launch_bounds__(256) xcorr_strip(const TileArgs a, const T* __restrict__ k, int nw, int flip) {
+// PARAM: the (flipped, row-padded) taps come in the kernel-parameter bank
+// (uniform constant loads, no shared-memory traffic: 13x13 fp64 10.9 -> 13.2
+// TFLOP/s against taps in shared memory), else they are staged from the device kernel
+// into shared memory (kernels larger than the 8 KB bank, graph capture
+// without a host copy of the kernel).
+template <typename T, int C, int VX, int TY, int TZ, bool PARAM>
+__global__ void __launch_bounds__(256) xcorr_strip(const TileArgs a, const T* __restrict__ k, int nw, int flip,
+                                                   const __grid_constant__ TapsParam<T> tp) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int nwp = (nw + C - 1) / C * C;  // padded taps per kernel row
   const int nrow_k = a.nz * a.ny;
   T* taps_smem = reinterpret_cast<T*>(smem_raw);
-  T* tile = taps_smem + ((size_t)nrow_k * nwp + 3) / 4 * 4;  // 16-byte aligned after the taps
+  T* tile = PARAM ? taps_smem : taps_smem + ((size_t)nrow_k * nwp + 3) / 4 * 4;  // 16-byte aligned after the taps
+  const T* taps = PARAM ? tp.v : taps_smem;
   const int tid = threadIdx.x, nthr = blockDim.x;
-  const int64_t kt = (int64_t)nrow_k * nw;
-  for (int idx = tid; idx < nrow_k * nwp; idx += nthr) {
-    const int row = idx / nwp, j2 = idx - row * nwp;
-    const int64_t t = (int64_t)row * nw + j2;
-    taps_smem[idx] = j2 < nw ? __ldg(k + (flip ? kt - 1 - t : t)) : T(0);  // padding is never multiplied
+  if (!PARAM) {
+    const int64_t kt = (int64_t)nrow_k * nw;
+    for (int idx = tid; idx < nrow_k * nwp; idx += nthr) {
+      const int row = idx / nwp, j2 = idx - row * nwp;
+      const int64_t t = (int64_t)row * nw + j2;
+      taps_smem[idx] = j2 < nw ? __ldg(k + (flip ? kt - 1 - t : t)) : T(0);  // padding is never multiplied
+    }
   }
   const int tx = tid % a.txn, ty = tid / a.txn;
   const int BX = a.txn * VX, BY = a.tyn * TY;
@@ -361,22 +370,27 @@ __global__ void __launch_bounds__(256) xcorr_strip(const TileArgs a, const T* __
       }
       __syncthreads();  // previous slice consumed (and the taps staged, first time)
       {
+        // staged tile, one warp per row (no index division per element)
         const T* sp = s + gz * plane;
         const int iy0 = y0 - a.py, ix0 = x0 - a.px;
-        const int total = a.sx * a.sy;
-        for (int idx = tid; idx < total; idx += nthr) {
-          const int r = idx / a.sx, c = idx - r * a.sx;
-          int gy = iy0 + r, gx = ix0 + c;
-          T v = T(0);
-          const bool in = (unsigned)gy < (unsigned)a.my && (unsigned)gx < (unsigned)a.mx;
-          if (in) {
-            v = __ldg(sp + (int64_t)gy * a.mx + gx);
-          } else if (a.boundary == CT_REPLICATE) {
-            gy = min(max(gy, 0), a.my - 1);
-            gx = min(max(gx, 0), a.mx - 1);
-            v = __ldg(sp + (int64_t)gy * a.mx + gx);
+        const int lane = tid & 31, nwarp = nthr >> 5;
+        for (int r = tid >> 5; r < a.sy; r += nwarp) {
+          int gy = iy0 + r;
+          const bool row_in = (unsigned)gy < (unsigned)a.my;
+          if (!row_in && a.boundary == CT_REPLICATE) gy = min(max(gy, 0), a.my - 1);
+          const T* srow = sp + (int64_t)gy * a.mx;
+          T* trow = tile + r * a.sx;
+          for (int c = lane; c < a.sx; c += 32) {
+            int gx = ix0 + c;
+            T v = T(0);
+            if (row_in && (unsigned)gx < (unsigned)a.mx) {
+              v = __ldg(srow + gx);
+            } else if (a.boundary == CT_REPLICATE) {
+              gx = min(max(gx, 0), a.mx - 1);
+              v = __ldg(srow + gx);
+            }
+            trow[c] = v;
           }
-          tile[idx] = v;
         }
       }
       __syncthreads();
@@ -384,9 +398,9 @@ __global__ void __launch_bounds__(256) xcorr_strip(const TileArgs a, const T* __
       for (int r = 0; r < nrows; ++r) {
         const T* rowp = tile + (ty * TY + r) * a.sx + tx * VX;
         for (int st = 0; st < full; ++st)
-          strip_fma<T, C, C, VX, TY, TZ>(rowp + st * C, taps_smem + st * C, nwp, izr, r, nz, ny, acc);
+          strip_fma<T, C, C, VX, TY, TZ>(rowp + st * C, taps + st * C, nwp, izr, r, nz, ny, acc);
         const T* rt = rowp + full * C;
-        const T* kt_ = taps_smem + full * C;
+        const T* kt_ = taps + full * C;
         switch (tail) {  // compile-time tail strip
 #define CT_TAIL(Wt) case Wt: strip_fma<T, Wt, C, VX, TY, TZ>(rt, kt_, nwp, izr, r, nz, ny, acc); break;
           CT_TAIL(1) CT_TAIL(2) CT_TAIL(3) CT_TAIL(4) CT_TAIL(5) CT_TAIL(6) CT_TAIL(7)
@@ -421,10 +435,10 @@ constexpr int kStripC = 8;  // compile-time taps per strip (a multiple of both v
 
 // smem bytes of xcorr_strip for these extents (0: does not fit one CTA)
 template <typename T>
-size_t strip_smem(const TileArgs& a, int nw, int txn, int tyn, int TY) {
+size_t strip_smem(const TileArgs& a, int nw, int txn, int tyn, int TY, bool param = false) {
   constexpr int VX = 16 / sizeof(T);
   const int nwp = (nw + kStripC - 1) / kStripC * kStripC;
-  const size_t taps = ((size_t)a.nz * a.ny * nwp + 3) / 4 * 4;
+  const size_t taps = param ? 0 : ((size_t)a.nz * a.ny * nwp + 3) / 4 * 4;
   const int BX = txn * VX, BY = tyn * TY;
   const int sx = BX - VX + (VX + nwp - 1 + VX - 1) / VX * VX;  // every strip's window loads stay in the row
   const size_t tile = (size_t)sx * (BY + a.ny - 1);
@@ -433,22 +447,28 @@ size_t strip_smem(const TileArgs& a, int nw, int txn, int tyn, int TY) {
 }
 
 template <typename T, int TY, int TZ>
-int launch_strip(const TileArgs& a0, const T* k_dev, int nw, int flip, cudaStream_t st) {
+int launch_strip(const TileArgs& a0, const T* k_dev, const T* taps_host, int nw, int flip, cudaStream_t st) {
   constexpr int VX = 16 / sizeof(T);
   TileArgs a = a0;
   a.txn = 32;
   a.tyn = 8;
-  const size_t smem = strip_smem<T>(a, nw, a.txn, a.tyn, TY);
-  CT_REQUIRE(smem > 0, "kernel too large for the strip kernel");
   const int nwp = (nw + kStripC - 1) / kStripC * kStripC;
+  // taps_host: the flipped taps in row-major order (nullptr: stage from k_dev)
+  const bool param = taps_host != nullptr && (int64_t)a.nz * a.ny * nwp <= MaxTaps<T>::value;
+  const size_t smem = strip_smem<T>(a, nw, a.txn, a.tyn, TY, param);
+  CT_REQUIRE(smem > 0, "kernel too large for the strip kernel");
   a.sx = a.txn * VX - VX + (VX + nwp - 1 + VX - 1) / VX * VX;
   a.sy = a.tyn * TY + a.ny - 1;
   a.tiles_z = TZ > 1 ? (int)cdiv(a.oz, TZ) : a.oz;
-  auto kern = xcorr_strip<T, kStripC, VX, TY, TZ>;
+  TapsParam<T> tp;
+  if (param)
+    for (int row = 0; row < a.nz * a.ny; ++row)
+      for (int j2 = 0; j2 < nwp; ++j2) tp.v[row * nwp + j2] = j2 < nw ? taps_host[row * nw + j2] : T(0);
+  auto kern = param ? xcorr_strip<T, kStripC, VX, TY, TZ, true> : xcorr_strip<T, kStripC, VX, TY, TZ, false>;
   CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 grid((unsigned)cdiv(a.ox, a.txn * VX), (unsigned)cdiv(a.oy, a.tyn * TY),
             (unsigned)std::min<int64_t>(a.batch * a.tiles_z, 65535));
-  kern<<<grid, a.txn * a.tyn, smem, st>>>(a, k_dev, nw, flip);
+  kern<<<grid, a.txn * a.tyn, smem, st>>>(a, k_dev, nw, flip, tp);
   return check_launch("xcorr_strip");
 }
 
@@ -1961,9 +1981,19 @@ int dispatch(int ndim, const void* s, const int64_t* ms, int64_t batch, const vo
     // rows per thread: fp64 reuses each window load over 8 output rows (the
     // DFMA:load ratio), fp32 over 4
     constexpr int STY = sizeof(T) == 8 ? CT_STRIP_TY64 : 4;
-    if (strip_smem<T>(a, nw, 32, 8, STY) > 0) {
-      if (is3d) return launch_strip<T, STY, 2>(a, reinterpret_cast<const T*>(k), nw, flip, st);
-      return launch_strip<T, STY, 1>(a, reinterpret_cast<const T*>(k), nw, flip, st);
+    // taps in the parameter bank when they fit and a host copy is at hand (or
+    // can be read: not while the stream is being captured)
+    const int nwp = (nw + kStripC - 1) / kStripC * kStripC;
+    T taps_h[MaxTaps<T>::value];  // flipped host taps (the launch copies the parameter block)
+    const T* th = nullptr;
+    if ((int64_t)a.nz * a.ny * nwp <= MaxTaps<T>::value && (k_host || cap == cudaStreamCaptureStatusNone)) {
+      int rc2 = taps_to_host<T>(k, k_host, k_elems, flip, taps_h, st);
+      if (rc2) return rc2;
+      th = taps_h;
+    }
+    if (strip_smem<T>(a, nw, 32, 8, STY, th != nullptr) > 0) {
+      if (is3d) return launch_strip<T, STY, 2>(a, reinterpret_cast<const T*>(k), th, nw, flip, st);
+      return launch_strip<T, STY, 1>(a, reinterpret_cast<const T*>(k), th, nw, flip, st);
     }
   }
   if (tiled_ok) {
