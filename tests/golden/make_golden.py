@@ -161,9 +161,32 @@ def gradient_fixtures():
     print("gradient fixtures done")
 
 
+def nonfinite_fixtures():
+    """NaN / Inf propagation through the hot path (the reference has no guard:
+    IEEE semantics of its numpy / numba arithmetic decide every field)."""
+    rng = np.random.default_rng(2718)
+    frames = generate(SynthConfig(width=64, height=48, frames=5, t0=40.0, foe=(0.45, 0.55), seed=3)).frames.copy()
+    frames[1, 10, 10] = np.nan
+    frames[3, 5, 7] = np.inf
+    out = {"frames": frames}
+    for key, kw in (("l0", dict(level=0)), ("l1", dict(level=1)), ("ms2", dict(max_level=2))):
+        out[key] = np.array([est_row(e) for e in rttc.run_sequence(frames, **kw)])
+    s = rng.random((20, 30))
+    s[4, 5] = np.nan
+    s[17, 0] = -np.inf
+    k = rng.standard_normal((3, 4))
+    out["conv_s"], out["conv_k"] = s, k
+    out["conv_full"] = conv_direct(s, k, ConvShape.FULL)
+    out["xcorr_same_rep"] = xcorr_direct(s, k, ConvShape.SAME, BoundaryPolicy.REPLICATE)
+    np.savez_compressed(os.path.join(HERE, "nonfinite_fixtures.npz"), **out)
+    print("nonfinite fixtures done")
+
+
+SECTIONS = {"gradient": lambda: gradient_fixtures(), "conv_cases": lambda: conv_cases(),
+            "ttc": lambda: ttc_fixtures(), "conv_configs": lambda: conv_configs(),
+            "nonfinite": lambda: nonfinite_fixtures()}
+
 if __name__ == "__main__":
     print("reference convtact", convtact.__version__)
-    gradient_fixtures()
-    conv_cases()
-    ttc_fixtures()
-    conv_configs()
+    for name in (sys.argv[1:] or SECTIONS):  # default: every fixture file
+        SECTIONS[name]()

@@ -127,3 +127,14 @@ def test_gradient_fixtures_restated(golden):
         assert np.array_equal(ex, g[f"{name}_ex"]) and np.array_equal(ey, g[f"{name}_ey"]), name
         assert np.array_equal(np.hypot(ex, ey), g[f"{name}_mag"]), name
         assert np.array_equal(np.arctan2(ey, ex), g[f"{name}_dir"]), name
+
+
+def test_nonfinite_fixtures_restated(golden):
+    """NaN / Inf inputs: the oracle reproduces the reference's IEEE propagation
+    field for field (fixtures from the reference itself, make_golden.py nonfinite)."""
+    z = golden("nonfinite_fixtures.npz")
+    for key, kw in (("l0", dict(level=0)), ("l1", dict(level=1)), ("ms2", dict(max_level=2))):
+        assert np.array_equal(O.run_sequence(z["frames"], **kw), z[key], equal_nan=True), key
+    assert np.array_equal(O.direct(z["conv_s"], z["conv_k"], "full"), z["conv_full"], equal_nan=True)
+    assert np.array_equal(O.direct(z["conv_s"], z["conv_k"], "same", "replicate", flip=False), z["xcorr_same_rep"],
+                          equal_nan=True)

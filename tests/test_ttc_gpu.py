@@ -528,3 +528,17 @@ def test_host_paths_pageable_and_pinned_match_device():
     est = ct.run_sequence(f32, level=0)
     want = ct.run_sequence_batch(torch.from_numpy(f32.astype(np.float64)).cuda()[None], level=0)[0].cpu().numpy()
     assert np.array_equal(rows(est)[:, :8], want[:, :8], equal_nan=True)
+
+
+def test_nonfinite_inputs_match_the_reference(golden):
+    """NaN / Inf pixels propagate exactly as in the reference (fixtures produced by
+    the reference itself): single-scale, level 1 and multiscale rows, and
+    convolution outputs, NaN positions and values identical."""
+    z = golden("nonfinite_fixtures.npz")
+    for key, kw in (("l0", dict(level=0)), ("l1", dict(level=1)), ("ms2", dict(max_level=2))):
+        got = np.array([[np.nan] * 8 + [-1.0, np.nan] if e is None else [float(getattr(e, f)) for f in EST]
+                        for e in ct.run_sequence(z["frames"], **kw)])
+        assert np.array_equal(got, z[key], equal_nan=True), key
+    assert np.array_equal(ct.conv_direct(z["conv_s"], z["conv_k"]), z["conv_full"], equal_nan=True)
+    assert np.array_equal(ct.xcorr_direct(z["conv_s"], z["conv_k"], ct.ConvShape.SAME, ct.BoundaryPolicy.REPLICATE),
+                          z["xcorr_same_rep"], equal_nan=True)
