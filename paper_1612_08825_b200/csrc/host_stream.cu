@@ -112,6 +112,7 @@ class CopyPool {
       memcpy(dst, src, bytes);
       return;
     }
+    std::lock_guard<std::mutex> call(call_mu_);  // one job at a time (callers on several host threads)
     {
       std::unique_lock<std::mutex> lk(mu_);
       dst_ = static_cast<char*>(dst);
@@ -151,7 +152,7 @@ class CopyPool {
     }
   }
   std::vector<std::thread> workers_;
-  std::mutex mu_;
+  std::mutex call_mu_, mu_;
   std::condition_variable cv_, done_;
   uint64_t gen_ = 0;
   int pending_ = 0;
