@@ -542,3 +542,21 @@ def test_nonfinite_inputs_match_the_reference(golden):
     assert np.array_equal(ct.conv_direct(z["conv_s"], z["conv_k"]), z["conv_full"], equal_nan=True)
     assert np.array_equal(ct.xcorr_direct(z["conv_s"], z["conv_k"], ct.ConvShape.SAME, ct.BoundaryPolicy.REPLICATE),
                           z["xcorr_same_rep"], equal_nan=True)
+
+
+def test_host_path_concurrent_callers():
+    """Two host threads streaming pageable videos at once (the copy pool and the
+    pinned rings are shared / per thread): each gets its own video's rows."""
+    from concurrent.futures import ThreadPoolExecutor
+    g = torch.Generator(device="cuda").manual_seed(9)
+    dev = torch.rand((4, 40, 256, 256), dtype=torch.float64, device="cuda", generator=g)
+    ref = ct.run_sequence_batch(dev, level=0).cpu().numpy()
+    vids = [dev[v:v + 1].cpu().numpy() for v in range(4)]
+
+    def work(v):
+        return ct.run_sequence_host(vids[v], level=0)
+
+    with ThreadPoolExecutor(2) as ex:
+        outs = list(ex.map(work, [0, 1, 2, 3, 0, 1, 2, 3]))
+    for k, o in enumerate(outs):
+        assert np.array_equal(o[0], ref[k % 4], equal_nan=True), k
