@@ -63,7 +63,11 @@ const char* ct_version(void);
  * the nearest edge sample (CT_REPLICATE).  `k` is the kernel in device
  * memory; `k_host` may be NULL or a host copy of the same taps, which lets the
  * register-tiled kernels take the taps through the parameter bank without a
- * device->host copy (and without synchronising the stream). */
+ * device->host copy (and without synchronising the stream).  Ranks 1-3 run on
+ * register-tiled kernels for every kernel width (compile-time widths 1-9, 11,
+ * 15, 31; any other width on the runtime-width strip kernel); ranks >= 4 on
+ * the one-thread-per-output kernel.  float64 results are bit-identical to the
+ * reference loops. */
 int ct_xcorr_nd(int dtype, int ndim, const void* s, const int64_t* s_shape, int64_t batch,
                 const void* k, const void* k_host, const int64_t* k_shape,
                 const int64_t* pad_left, const int64_t* out_shape, int boundary, void* out,
@@ -136,7 +140,11 @@ int ct_run_sequence(int dtype, const void* frames, int64_t n_videos, int64_t n_f
 
 /* run_sequence from HOST frames (f64 or f32 host buffer), streaming them to
  * the device in chunks that overlap the copy with compute; est_host receives
- * [n_videos][n_frames-1][10].  Device workspace via the query below. */
+ * [n_videos][n_frames-1][10].  Device workspace via the query below.
+ * Page-locked frames are copied directly; pageable frames (a plain numpy
+ * array) are staged through a page-locked ring of two 8 MB slots owned by the
+ * library (one per calling host thread, reused across calls), filled by a
+ * small pool of host copy threads while the previous chunk crosses PCIe. */
 size_t ct_run_sequence_host_workspace_bytes(int dtype, int64_t n_videos, int64_t n_frames,
                                             int64_t h, int64_t w, int level, int max_level);
 int ct_run_sequence_host(int dtype, const void* frames_host, int64_t n_videos, int64_t n_frames,
