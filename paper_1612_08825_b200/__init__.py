@@ -21,6 +21,7 @@ from .conv import (
     reflect,
     xcorr_direct,
 )
+from .ingest import FormatError, image_read_pgm, image_write_pgm, tensor_read
 from .kernels import KERNELS, GradientField, NamedKernel, gradient, kernel_lookup
 from .synth import (
     ScoreReport,
@@ -32,6 +33,7 @@ from .synth import (
     make_texture_device,
     make_textures,
     score_mse,
+    write_sequence,
     zoom_frame,
     zoom_frames,
 )

@@ -109,6 +109,22 @@ def decode_on_device(raw: torch.Tensor, maxval: int, shape) -> torch.Tensor:
     return out
 
 
+def image_write_pgm(img, path) -> None:
+    """tensor.image_write_pgm (tensor.py:139-148): an [h, w] image as 8-bit binary
+    PGM, values clamped to [0, 1] and rounded half to even.  Host I/O (a CUDA
+    tensor is copied back first)."""
+    if isinstance(img, torch.Tensor):
+        img = img.detach().cpu().numpy()
+    img = np.asarray(img, dtype=np.float64)
+    if img.ndim != 2:
+        raise ValueError(f"image must be 2-D, got ndim {img.ndim}")
+    h, w = img.shape
+    q = np.rint(np.clip(img, 0.0, 1.0) * 255.0).astype(np.uint8)
+    with open(path, "wb") as f:
+        f.write(f"P5\n{w} {h}\n255\n".encode("ascii"))
+        f.write(q.tobytes(order="C"))
+
+
 def image_read_pgm(path):
     """tensor.image_read_pgm with the decode on the device; returns a float64 numpy image."""
     raw, maxval = read_pgm_raw(path)

@@ -161,6 +161,26 @@ def generate(cfg: SynthConfig, device: bool = False, dtype=torch.float64) -> Syn
     return SyntheticSequence(frames=out, truth=truth, config=cfg)
 
 
+TRUTH_HEADER = "frame,ttc,foe_x,foe_y"
+
+
+def write_sequence(seq: SyntheticSequence, outdir) -> None:
+    """synth.write_sequence (synth.py:149-162): frame_%06d.pgm per frame plus
+    truth.csv (host I/O; device frames are copied back)."""
+    from pathlib import Path
+
+    from .ingest import image_write_pgm
+    out = Path(outdir)
+    out.mkdir(parents=True, exist_ok=True)
+    frames = seq.frames.detach().cpu().numpy() if isinstance(seq.frames, torch.Tensor) else seq.frames
+    for t in range(frames.shape[0]):
+        image_write_pgm(frames[t], out / f"frame_{t:06d}.pgm")
+    lines = [TRUTH_HEADER] + [f"{int(r[0])},{format(r[1], '.17g')},{format(r[2], '.17g')},{format(r[3], '.17g')}"
+                              for r in seq.truth]
+    with open(out / "truth.csv", "w", newline="\n") as f:
+        f.write("\n".join(lines) + "\n")
+
+
 @dataclass(frozen=True)
 class ScoreReport:
     mse: float

@@ -46,3 +46,26 @@ def test_synthetic_sequence_fields():
     assert tuple(ct.SyntheticSequence.__dataclass_fields__) == ("frames", "truth", "config")
     seq = ct.SyntheticSequence(frames=np.zeros((2, 16, 16)), truth=np.zeros((2, 4)), config=ct.SynthConfig(frames=2))
     assert seq.config.frames == 2
+
+
+def test_image_write_pgm_and_write_sequence(tmp_path):
+    # tensor.image_write_pgm (tensor.py:139-148) and synth.write_sequence (synth.py:149-162): host I/O
+    img = np.array([[0.0, 0.5 / 255, 1.5 / 255, 1.0], [-1.0, 2.0, 0.25, 0.75]])
+    ct.image_write_pgm(img, tmp_path / "a.pgm")
+    raw = (tmp_path / "a.pgm").read_bytes()
+    assert raw.startswith(b"P5\n4 2\n255\n")
+    assert list(raw[len(b"P5\n4 2\n255\n"):]) == [0, 0, 2, 255, 0, 255, 64, 191]  # clamp, round half to even
+    with pytest.raises(ValueError):
+        ct.image_write_pgm(np.zeros(3), tmp_path / "b.pgm")
+    cfg = ct.SynthConfig(width=16, height=16, frames=3, t0=10.0)
+    frames = np.random.default_rng(1).random((3, 16, 16))
+    truth = np.array([(t, 10.0 - t, 6.4, 8.8) for t in range(3)])
+    seq = ct.SyntheticSequence(frames=frames, truth=truth, config=cfg)
+    ct.write_sequence(seq, tmp_path / "s1")
+    ct.write_sequence(seq, tmp_path / "s2")
+    names = sorted(p.name for p in (tmp_path / "s1").iterdir())
+    assert names == ["frame_000000.pgm", "frame_000001.pgm", "frame_000002.pgm", "truth.csv"]
+    for n in names:
+        assert (tmp_path / "s1" / n).read_bytes() == (tmp_path / "s2" / n).read_bytes()
+    lines = (tmp_path / "s1" / "truth.csv").read_text().splitlines()
+    assert lines[0] == "frame,ttc,foe_x,foe_y" and lines[1] == "0,10,6.4000000000000004,8.8000000000000007"
