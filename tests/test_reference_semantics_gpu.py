@@ -164,6 +164,10 @@ def test_criterion_12_determinism(clean, tmp_path):
     assert np.array_equal(again.frames, suite[1].frames) and np.array_equal(again.truth, suite[1].truth)
     cfg = SynthConfig(seed=2, noise_sigma=0.05)
     assert np.array_equal(ct.generate(cfg).frames, ct.generate(cfg).frames)
+    ct.write_sequence(again, tmp_path / "d1")
+    ct.write_sequence(again, tmp_path / "d2")
+    for name in ("truth.csv", "frame_000000.pgm", "frame_000059.pgm"):
+        assert (tmp_path / "d1" / name).read_bytes() == (tmp_path / "d2" / name).read_bytes()
     ct.write_trace(ct.run_sequence(again.frames[:10], level=0), tmp_path / "a.csv")
     ct.write_trace(ct.run_sequence(torch.from_numpy(again.frames[:10]).cuda(), level=0), tmp_path / "b.csv")
     assert (tmp_path / "a.csv").read_bytes() == (tmp_path / "b.csv").read_bytes()
