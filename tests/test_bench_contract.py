@@ -39,3 +39,22 @@ def test_reference_arm_json_line():
 def test_gpu_arm_fails_loudly_without_a_device():
     r = run_bench("--steps", "1", "--warmup", "3", "--no-secondary")
     assert r.returncode != 0
+
+
+def test_reference_arm_under_torchrun_prints_one_line_from_rank0():
+    # the driver launches the reference arm like the GPU arm (torchrun, N ranks):
+    # rank 0 alone runs and prints; the other ranks exit 0 without work
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                        "--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "3", "--ref-videos", "1",
+                        "--quick"], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
