@@ -325,7 +325,7 @@ DP_PER_PX = 711.539e6 * 32 / (256 * 63 * 255 * 255)  # ncu FP64 warp instruction
 def fma_peaks():
     """FP32 (FFMA) and FP64 (DFMA) TFLOP/s measured in this run by the FMA-chain
     probe (tools/fp_peak_lib.cu, built by __graft_entry__.build()), plus the
-    theoretical peaks at the SM clock NVML reports (148 SMs x 128 / 64 lanes x 2)."""
+    theoretical peaks at the maximum SM clock NVML reports (148 SMs x 128 / 64 lanes x 2)."""
     import ctypes
     import torch
     out = {}
@@ -344,8 +344,10 @@ def fma_peaks():
     try:
         import pynvml
         pynvml.nvmlInit()
-        mhz = pynvml.nvmlDeviceGetClockInfo(pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device()),
-                                            pynvml.NVML_CLOCK_SM)
+        # the maximum SM clock (the hardware limit the kernels are rated against;
+        # the instantaneous clock after a long run can sit lower)
+        mhz = pynvml.nvmlDeviceGetMaxClockInfo(pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device()),
+                                               pynvml.NVML_CLOCK_SM)
     except Exception:
         mhz = 1965
     out["theoretical_at_clock"] = {"sm_mhz": mhz, "fp32": sms * 128 * 2 * mhz * 1e6 / 1e12,
@@ -362,7 +364,7 @@ def secondary_configs(quick: bool, peaks):
     # FMA-chain rate measured in this run is reported beside it (frac_vs_measured_rate)
     p32, p64 = peaks["theoretical_at_clock"]["fp32"], peaks["theoretical_at_clock"]["fp64"]
     m32, m64 = peaks["fp32"], peaks["fp64"]
-    pnote = ("theoretical FMA peak at the SM clock: 148 SMs x %s lanes x 2 flop x %d MHz"
+    pnote = ("theoretical FMA peak at the maximum SM clock: 148 SMs x %s lanes x 2 flop x %d MHz"
              % ("{128 fp32 | 64 fp64}", peaks["theoretical_at_clock"]["sm_mhz"]))
     st = torch.cuda.current_stream()
 
@@ -615,7 +617,7 @@ def main():
                           "achieved_lane_ops_per_s": DP_PER_PX * V * (NFRAMES - 1) * 255 * 255 / t_k,
                           "peak_lane_ops_per_s": fp64_lane_peak,
                           "frac": DP_PER_PX * V * (NFRAMES - 1) * 255 * 255 / t_k / fp64_lane_peak,
-                          "peak_note": "theoretical DFMA rate at the SM clock (148 x 64 lanes x MHz)",
+                          "peak_note": "theoretical DFMA rate at the maximum SM clock (148 x 64 lanes x MHz)",
                           "frac_vs_measured_rate": DP_PER_PX * V * (NFRAMES - 1) * 255 * 255 / t_k / (peaks["fp64"] * 1e12 / 2)},
             "hbm_read_only_probe_gbs": 7500, "hbm_read_only_note": "TMA stream of the same boxes/ring/grid without compute (tools/tma_stream2.cu); above the copy peak"}
 
