@@ -560,3 +560,20 @@ def test_host_path_concurrent_callers():
         outs = list(ex.map(work, [0, 1, 2, 3, 0, 1, 2, 3]))
     for k, o in enumerate(outs):
         assert np.array_equal(o[0], ref[k % 4], equal_nan=True), k
+
+
+def test_4k_frames_multiscale_every_field():
+    """Larger than config 5: 2160 x 3840 fp32 frames (16 column tiles, five
+    pyramid levels), two pairs against the oracle on the rounded frames; the
+    same field tolerances as the 1080p config-5 test."""
+    import paper_1612_08825_b200.synth as S
+    fr, _ = S.approach_stream(3, 2160, 3840, seed=77, dtype=torch.float32)
+    got = ct.run_sequence_batch(fr[None], max_level=4).cpu().numpy()[0]
+    ref = O.run_sequence(fr.cpu().numpy().astype(np.float64), max_level=4)
+    assert np.array_equal(got[:, 8], ref[:, 8]) and np.array_equal(got[:, 9], ref[:, 9])
+    errs = field_errors(got, ref)
+    assert errs["c"] <= CFG5_TOL["c"] and errs["ttc"] <= CFG5_TOL["ttc"], errs
+    assert errs["residual"] <= CFG5_TOL["residual"] and errs["misfit"] <= CFG5_TOL["misfit"], errs
+    fin = np.isfinite(ref[:, 2]) & (ref[:, 9] == 0)
+    assert np.all(np.abs(got[fin, 3] - ref[fin, 3]) <= CFG5_FOE_PX * 2 ** ref[fin, 8])
+    assert np.all(np.abs(got[fin, 4] - ref[fin, 4]) <= CFG5_FOE_PX * 2 ** ref[fin, 8])
