@@ -441,6 +441,9 @@ __global__ void __launch_bounds__(256) xcorr_strip(const TileArgs a, const T* __
 #ifndef CT_STRIP_VX64
 #define CT_STRIP_VX64 2
 #endif
+#ifndef CT_STRIP_TY32
+#define CT_STRIP_TY32 4
+#endif
 constexpr int kStripC = 8;  // compile-time taps per strip (a multiple of both vector widths)
 template <typename T>
 constexpr int strip_vx() {  // outputs per thread along x
@@ -2037,7 +2040,7 @@ int dispatch(int ndim, const void* s, const int64_t* ms, int64_t batch, const vo
     const bool is3d = a.oz > 1 || a.nz > 1;
     // rows per thread: fp64 reuses each window load over 8 output rows (the
     // DFMA:load ratio), fp32 over 4
-    constexpr int STY = sizeof(T) == 8 ? CT_STRIP_TY64 : 4;
+    constexpr int STY = sizeof(T) == 8 ? CT_STRIP_TY64 : CT_STRIP_TY32;
     // taps in the parameter bank when they fit and a host copy is at hand (or
     // can be read: not while the stream is being captured)
     const int nwp = (nw + kStripC - 1) / kStripC * kStripC;
