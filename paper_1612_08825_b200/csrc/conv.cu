@@ -839,13 +839,52 @@ int launch_tma3d(const TileArgs& a0, const T* taps_host, int ntaps, cudaStream_t
 // taps come from the parameter bank with a uniform offset, and each staged
 // value feeds NZ * TY * NW FMAs.  Per output the taps are still applied in
 // row-major (j0, j1, j2) order from 0.0, so fp64 results are bit-exact.
+// Work split of the z-walking kernels.  nc > 0: every (volume, tile) column is
+// cut into nc runs of consecutive output slices [zb[i], zb[i+1]) of equal
+// WORK -- an output slice costs one kernel plane per input slice that exists,
+// so the first and last NZ-1 slices of a FULL-mode column are cheaper -- and
+// CTA c takes run c % nc of column c / nc: one run per CTA (one pipeline
+// fill), no run straddling two columns.  nc == 0: the flattened (column, z)
+// slices in equal counts per CTA (more columns than CTA slots).
+constexpr int kMaxZRuns = 32;
+struct ZRuns {
+  int nc;
+  int zb[kMaxZRuns + 1];
+};
+
+inline ZRuns plan_zruns(const TileArgs& a, int nz, int64_t columns, int64_t slots) {
+  ZRuns r;
+  memset(&r, 0, sizeof(r));
+  if (getenv("CT_ZW_FLAT")) return r;  // probing only
+  int64_t nc = columns > 0 ? slots / columns : 0;
+  nc = std::min<int64_t>(nc, std::min<int64_t>(kMaxZRuns, a.oz / (2 * nz)));
+  if (nc < 1 || (double)(nc * columns) < 0.9 * (double)slots) return r;
+  std::vector<int64_t> pre(a.oz + 1, 0);  // work prefix: planes with an existing input slice
+  for (int z = 0; z < a.oz; ++z) {
+    const int lo = std::max(0, z - a.pz), hi = std::min(a.mz, z - a.pz + nz);
+    pre[z + 1] = pre[z] + std::max(0, hi - lo) + 1;  // + 1: the per-slice store / bookkeeping
+  }
+  r.nc = (int)nc;
+  int z = 0;
+  for (int i = 1; i < nc; ++i) {
+    const double target = (double)pre[a.oz] * i / (double)nc;
+    while (z < a.oz && (double)pre[z + 1] <= target) ++z;
+    // the nearer of pre[z], pre[z + 1]
+    if (z < a.oz && target - (double)pre[z] > (double)pre[z + 1] - target) ++z;
+    r.zb[i] = std::max(z, r.zb[i - 1] + 1);
+  }
+  r.zb[nc] = a.oz;
+  for (int i = (int)nc - 1; i > 0; --i) r.zb[i] = std::min(r.zb[i], r.zb[i + 1] - 1);
+  return r;
+}
+
 #ifndef CT_ZW_WARP_REL
 #define CT_ZW_WARP_REL 1  // per-warp stage release (0: CTA barrier per slice, the round-1 kernel)
 #endif
 template <typename T, int NZ, int NH, int NW, int TY, int VX, int LW, int MAXT>
 __global__ void __launch_bounds__(MAXT, 1) xcorr_zwalk(const TileArgs a, const __grid_constant__ TapsParam<T> taps,
                                                       const __grid_constant__ CUtensorMap tmap, int pxa,
-                                                      int64_t per_cta) {
+                                                      int64_t per_cta, const __grid_constant__ ZRuns zr) {
   extern __shared__ __align__(128) unsigned char smem_zw[];
   constexpr int NS = 3;                             // TMA ring stages
   constexpr int CW = VX + NW - 1;                   // window columns per row
@@ -868,7 +907,12 @@ __global__ void __launch_bounds__(MAXT, 1) xcorr_zwalk(const TileArgs a, const _
   const bool active = ty < a.tyn;
   const int64_t total = a.batch * tiles_y * tiles_x * (int64_t)a.oz;
   int64_t pos = (int64_t)blockIdx.x * per_cta;
-  const int64_t end = min(total, pos + per_cta);
+  int64_t end = min(total, pos + per_cta);
+  if (zr.nc > 0) {  // run blockIdx.x % nc of column blockIdx.x / nc
+    const int64_t c0 = (int64_t)(blockIdx.x / zr.nc) * a.oz;
+    pos = c0 + zr.zb[blockIdx.x % zr.nc];
+    end = c0 + zr.zb[blockIdx.x % zr.nc + 1];
+  }
   if (tid == 0) {
     for (int i = 0; i < NS; ++i) mbar_init(&bars[i], 1);
 #if CT_ZW_WARP_REL
@@ -1075,7 +1119,7 @@ int launch_zwalk(const TileArgs& a0, const T* taps_host, int ntaps, int zc_hint,
   const size_t smem = 3 * stage_bytes + 64;
   CT_REQUIRE(smem <= 227 * 1024, "zwalk tile too large");
   const int nthr = (int)cdiv(a.txn * a.tyn, 32) * 32;
-  void (*kern)(const TileArgs, const TapsParam<T>, const CUtensorMap, int, int64_t);
+  void (*kern)(const TileArgs, const TapsParam<T>, const CUtensorMap, int, int64_t, const ZRuns);
   if (VW == 4 && sh % 4 == 0 && VX % 4 == 0)
     kern = xcorr_zwalk<T, NZ, NH, NW, TY, VX, (VW == 4 ? 4 : 2), MAXT>;
   else if (sh % 2 == 0)
@@ -1091,8 +1135,13 @@ int launch_zwalk(const TileArgs& a0, const T* taps_host, int ntaps, int zc_hint,
   const int64_t slots = (int64_t)num_sms() * std::max(1, per_sm);
   int64_t per_cta = std::max<int64_t>(cdiv(total, slots), 2 * NZ);
   if (zc_hint > 0) per_cta = zc_hint;
-  if (const char* e = getenv("CT_ZW_ZC")) per_cta = std::max(1, atoi(e));  // probing only
-  const int64_t nctas = cdiv(total, per_cta);
+  ZRuns zr = plan_zruns(a, NZ, total / a.oz, slots);
+  if (zc_hint > 0) zr.nc = 0;
+  if (const char* e = getenv("CT_ZW_ZC")) {  // probing only
+    per_cta = std::max(1, atoi(e));
+    zr.nc = 0;
+  }
+  const int64_t nctas = zr.nc > 0 ? (total / a.oz) * zr.nc : cdiv(total, per_cta);
   CT_REQUIRE(nctas < (1ll << 31), "too many z-walk CTAs");
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof(tmap));
@@ -1103,9 +1152,9 @@ int launch_zwalk(const TileArgs& a0, const T* taps_host, int ntaps, int zc_hint,
     return CT_EUNSUPPORTED;
   }
   if (getenv("CT_DEBUG"))
-    fprintf(stderr, "xcorr_zwalk TY %d MAXT %d: tile %dx%d (%d thr) per_cta %lld per_sm %d ctas %lld smem %zu\n", TY,
-            MAXT, BX, BY, nthr, (long long)per_cta, per_sm, (long long)nctas, smem);
-  kern<<<(unsigned)nctas, nthr, smem, st>>>(a, taps, tmap, pxa, per_cta);
+    fprintf(stderr, "xcorr_zwalk TY %d MAXT %d: tile %dx%d (%d thr) per_cta %lld runs/column %d per_sm %d ctas %lld smem %zu\n",
+            TY, MAXT, BX, BY, nthr, (long long)per_cta, zr.nc, per_sm, (long long)nctas, smem);
+  kern<<<(unsigned)nctas, nthr, smem, st>>>(a, taps, tmap, pxa, per_cta, zr);
   return check_launch("xcorr_zwalk");
 }
 
@@ -1506,6 +1555,280 @@ int launch_zwalk_x2(const TileArgs& a0, const float* taps_host, int ntaps, cudaS
   return check_launch("xcorr_zwalk_x2");
 }
 
+// fp32 z-walking kernel with FFMA2 over pairs of kernel PLANES (config 3).
+// Same schedule as xcorr_zwalk (persistent runs of output slices, 3-stage TMA
+// slice ring released per warp, one output row x 8 columns per thread), but the
+// NZ register slots of a column are kept as float2 pairs of z-adjacent slots:
+// one staged value v feeds slots (j, j+1) with taps (k[j], k[j+1]), which is
+// exactly FFMA2's (scalar broadcast) x (packed pair from a uniform register
+// pair) + (packed accumulator) form -- no operand pair is ever built by moves,
+// the staged layout stays the plain TMA tile, and 7 planes cost 3 FFMA2 + 1
+// FFMA issue slots instead of 7.  The slots advance by one per slice, so the
+// pairing alternates: per column e[0..NZ] (NZ odd),
+//   even slice: slot j = e[j];           pairs (e0,e1)(e2,e3).. take (k0,k1)(k2,k3)..,
+//               e[NZ-1] takes k[NZ-1] alone and is complete afterwards;
+//   odd slice:  slot j = e[j-1], slot 0 = e[NZ]; pairs take (k1,k2)(k3,k4)..,
+//               e[NZ] takes k0 alone, e[NZ-2] is complete afterwards;
+//   then e' = [0, e[NZ], e0, .., e[NZ-3], 0] (two pair moves per column per
+//   two slices).
+// The parameter bank holds both tap orders per (j1, j2).  Slices at the ends of
+// a run (not every slot live) take a scalar path with per-slot predicates.
+template <int NZ, int SH4, int MAXT>
+__global__ void __launch_bounds__(MAXT, 1) xcorr_zwalk_zp(const TileArgs a, const __grid_constant__ TapsParam<float> taps,
+                                                         const __grid_constant__ CUtensorMap tmap, int pxa,
+                                                         int64_t per_cta, const __grid_constant__ ZRuns zr) {
+  static_assert(NZ % 2 == 1, "plane pairs need an odd plane count");
+  extern __shared__ __align__(128) unsigned char smem_zp[];
+  constexpr int NS = 3;
+  constexpr int VX = 8, NH = NZ, NW = NZ;
+  constexpr int NP = NZ / 2;                        // full pairs; P[NP] = (e[NZ-1], e[NZ])
+  constexpr int EP = (NZ + 1 + 3) / 4 * 4;          // floats per tap row
+  constexpr int NV4 = (SH4 + VX + NW - 1 + 3) / 4;  // 16-byte loads per window row
+  const int tid = threadIdx.x;
+  const int tx = tid % a.txn, ty = tid / a.txn;
+  const int BX = a.txn * VX, BY = a.tyn;
+  const int tiles_x = (a.ox + BX - 1) / BX, tiles_y = (a.oy + BY - 1) / BY;
+  const int sh = pxa - a.px;
+  const size_t stage_bytes = ((size_t)a.sx * a.sy * sizeof(float) + 127) & ~size_t(127);
+  auto stage = [&](int s) { return reinterpret_cast<float*>(smem_zp + (size_t)s * stage_bytes); };
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_zp + NS * stage_bytes);
+  int* rel = reinterpret_cast<int*>(smem_zp + NS * stage_bytes + 8 * NS);
+  const int nwarps = (int)(blockDim.x >> 5), lane = tid & 31;
+  const uint32_t box_bytes = (uint32_t)(a.sx * a.sy * sizeof(float));
+  const bool active = ty < a.tyn;
+  const int64_t total = a.batch * tiles_y * tiles_x * (int64_t)a.oz;
+  int64_t pos = (int64_t)blockIdx.x * per_cta;
+  int64_t end = min(total, pos + per_cta);
+  if (zr.nc > 0) {  // run blockIdx.x % nc of column blockIdx.x / nc
+    const int64_t c0 = (int64_t)(blockIdx.x / zr.nc) * a.oz;
+    pos = c0 + zr.zb[blockIdx.x % zr.nc];
+    end = c0 + zr.zb[blockIdx.x % zr.nc + 1];
+  }
+  if (tid == 0) {
+    for (int i = 0; i < NS; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i < NS; ++i) rel[i] = 0;
+    mbar_fence_init();
+  }
+  __syncthreads();
+  int gcount = 0;
+  const int wb = ty * a.sx + sh + tx * VX - SH4;  // aligned window base within a staged row
+
+  while (pos < end) {
+    const int64_t col = pos / a.oz;
+    const int z0 = (int)(pos - col * a.oz);
+    const int64_t left = end - pos;
+    const int z1 = left < (int64_t)(a.oz - z0) ? z0 + (int)left : a.oz;
+    pos += z1 - z0;
+    const int b = (int)(col / (tiles_x * tiles_y));
+    const int tt = (int)(col - (int64_t)b * tiles_x * tiles_y);
+    const int x0 = (tt % tiles_x) * BX, y0 = (tt / tiles_x) * BY;
+    const int s_beg = z0 - a.pz, s_end = z1 - a.pz + NZ - 1;
+    const int g_lo = max(0, s_beg), g_hi = min(a.mz, s_end);
+    const int nsl = max(0, g_hi - g_lo);
+    const int g0 = gcount;
+    auto issue = [&](int k, bool any = false) {
+      if (any || tid == 0) {
+        const int st = (g0 + k) % NS;
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&bars[st], box_bytes);
+        tma_load_4d(stage(st), &tmap, &bars[st], x0 - pxa, y0 - a.py, g_lo + k, b);
+      }
+    };
+    for (int k = 0; k < NS && k < nsl; ++k) issue(k);
+
+    float2 P[NP + 1][VX];
+#pragma unroll
+    for (int i = 0; i <= NP; ++i)
+#pragma unroll
+      for (int x = 0; x < VX; ++x) P[i][x] = make_float2(0.f, 0.f);
+
+    float* out = reinterpret_cast<float*>(a.out) + (int64_t)b * a.oz * a.oy * a.ox;
+    const int ox = x0 + tx * VX;
+    const int oy = y0 + ty;
+
+    // one input slice s of parity PAR (0: slot j = e[j]; 1: slot j = e[j-1], slot 0 = e[NZ])
+    auto slice = [&](int s, auto par_c) {
+      constexpr int PAR = decltype(par_c)::value;
+      if (s >= g_lo && s < g_hi) {
+        const int k = s - g_lo;
+        const int g = g0 + k;
+        mbar_wait(&bars[g % NS], (uint32_t)((g / NS) & 1));
+        const int jlo = max(0, s + a.pz - z1 + 1), jhi = min(NZ - 1, s + a.pz - z0);
+        const float* tile = stage(g % NS) + wb;
+        const float* kpar = taps.v + PAR * (NH * NW * EP);
+        if (active) {
+          if (jlo == 0 && jhi == NZ - 1) {  // every slot live: plane pairs
+#pragma unroll 1
+            for (int j1 = 0; j1 < NH; ++j1) {
+              float v[NV4 * 4];
+              const float4* rp = reinterpret_cast<const float4*>(tile + j1 * a.sx);
+#pragma unroll
+              for (int c = 0; c < NV4; ++c) {
+                const float4 q = rp[c];
+                v[4 * c] = q.x;
+                v[4 * c + 1] = q.y;
+                v[4 * c + 2] = q.z;
+                v[4 * c + 3] = q.w;
+              }
+              const float* kj1 = kpar + j1 * (NW * EP);
+#pragma unroll
+              for (int j2 = 0; j2 < NW; ++j2) {
+                float kr[EP];
+#pragma unroll
+                for (int q = 0; q < EP; q += 4)
+                  *reinterpret_cast<float4*>(kr + q) = *reinterpret_cast<const float4*>(kj1 + j2 * EP + q);
+                const float ks = PAR ? kr[NZ] : kr[NZ - 1];
+#pragma unroll
+                for (int x = 0; x < VX; ++x) {
+                  const float vv = v[SH4 + x + j2];
+                  const float2 vb = make_float2(vv, vv);
+#pragma unroll
+                  for (int i = 0; i < NP; ++i) P[i][x] = ffma2(vb, make_float2(kr[2 * i], kr[2 * i + 1]), P[i][x]);
+                  if (PAR)
+                    P[NP][x].y = fmaf(ks, vv, P[NP][x].y);
+                  else
+                    P[NP][x].x = fmaf(ks, vv, P[NP][x].x);
+                }
+              }
+            }
+          } else {  // run ends: only slots jlo..jhi are live
+#pragma unroll 1
+            for (int j1 = 0; j1 < NH; ++j1) {
+              float v[NV4 * 4];
+              const float4* rp = reinterpret_cast<const float4*>(tile + j1 * a.sx);
+#pragma unroll
+              for (int c = 0; c < NV4; ++c) {
+                const float4 q = rp[c];
+                v[4 * c] = q.x;
+                v[4 * c + 1] = q.y;
+                v[4 * c + 2] = q.z;
+                v[4 * c + 3] = q.w;
+              }
+              const float* kj1 = kpar + j1 * (NW * EP);
+#pragma unroll
+              for (int j = 0; j < NZ; ++j) {
+                if (j < jlo || j > jhi) continue;
+                const int e = PAR ? (j == 0 ? NZ : j - 1) : j;  // register element of slot j (also its tap column)
+#pragma unroll
+                for (int j2 = 0; j2 < NW; ++j2) {
+                  const float kv = kj1[j2 * EP + e];
+#pragma unroll
+                  for (int x = 0; x < VX; ++x) {
+                    const float vv = v[SH4 + x + j2];
+                    if (e & 1)
+                      P[e >> 1][x].y = fmaf(kv, vv, P[e >> 1][x].y);
+                    else
+                      P[e >> 1][x].x = fmaf(kv, vv, P[e >> 1][x].x);
+                  }
+                }
+              }
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence_block();
+          if ((atomicAdd(&rel[g % NS], 1) % nwarps) == nwarps - 1 && k + NS < nsl) issue(k + NS, true);
+        }
+      }
+      // slot NZ-1 now holds output z = s + pz - (NZ-1), complete
+      const int zo = s + a.pz - (NZ - 1);
+      if (zo >= z0 && zo < z1 && active && oy < a.oy) {
+        float* orow = out + ((int64_t)zo * a.oy + oy) * a.ox;
+#pragma unroll
+        for (int x = 0; x < VX; ++x)
+          if (ox + x < a.ox) orow[ox + x] = PAR ? P[NP - 1][x].y : P[NP][x].x;
+      }
+    };
+
+    for (int s = s_beg; s < s_end; s += 2) {
+      slice(s, std::integral_constant<int, 0>{});
+      if (s + 1 < s_end) slice(s + 1, std::integral_constant<int, 1>{});
+      // e' = [0, e[NZ], e0, .., e[NZ-3], 0]
+#pragma unroll
+      for (int x = 0; x < VX; ++x) {
+        const float carry = P[NP][x].y;
+        P[NP][x] = make_float2(P[NP - 1][x].x, 0.f);
+#pragma unroll
+        for (int i = NP - 1; i > 0; --i) P[i][x] = P[i - 1][x];
+        P[0][x] = make_float2(0.f, carry);
+      }
+    }
+    gcount += nsl;
+    __syncthreads();  // run boundary: every stage free before the next run's first loads
+  }
+}
+
+template <int NZ, int MAXT = 256>
+int launch_zwalk_zp(const TileArgs& a0, const float* taps_host, int ntaps, cudaStream_t st) {
+  TileArgs a = a0;
+  constexpr int VX = 8, NH = NZ, NW = NZ;
+  constexpr int EP = (NZ + 1 + 3) / 4 * 4;
+  static_assert(2 * NH * NW * EP <= MaxTaps<float>::value, "tap rows exceed the parameter block");
+  TapsParam<float> taps;
+  memset(&taps, 0, sizeof(taps));
+  (void)ntaps;
+  for (int j1 = 0; j1 < NH; ++j1)
+    for (int j2 = 0; j2 < NW; ++j2) {
+      float* even = taps.v + (j1 * NW + j2) * EP;
+      float* odd = taps.v + NH * NW * EP + (j1 * NW + j2) * EP;
+      for (int j = 0; j < NZ; ++j) {
+        const float kv = taps_host[(j * NH + j1) * NW + j2];
+        even[j] = kv;
+        odd[j == 0 ? NZ : j - 1] = kv;
+      }
+    }
+  a.txn = a.tyn = 0;
+  choose_zwalk_tile(a.oy, a.ox, VX, 1, NH, NW, &a.txn, &a.tyn, MAXT);
+  if (getenv("CT_ZW_TXN") && getenv("CT_ZW_TYN")) {  // probing only
+    a.txn = atoi(getenv("CT_ZW_TXN"));
+    a.tyn = atoi(getenv("CT_ZW_TYN"));
+  }
+  const int pxa = (a.px + 3) / 4 * 4;
+  const int sh = pxa - a.px;  // 0..3
+  const int BX = a.txn * VX, BY = a.tyn;
+  const int nv4 = (sh + VX + NW - 1 + 3) / 4;
+  a.sx = std::max((sh + BX + NW - 1 + 3) / 4 * 4, BX - VX + 4 * nv4);  // every thread's vector loads stay in the row
+  a.sy = BY + NH - 1;
+  const size_t stage_bytes = ((size_t)a.sx * a.sy * sizeof(float) + 127) & ~size_t(127);
+  const size_t smem = 3 * stage_bytes + 64;
+  CT_REQUIRE(smem <= 227 * 1024, "zwalk tile too large");
+  const int nthr = (int)cdiv(a.txn * a.tyn, 32) * 32;
+  void (*kern)(const TileArgs, const TapsParam<float>, const CUtensorMap, int, int64_t, const ZRuns);
+  switch (sh) {
+    case 0: kern = xcorr_zwalk_zp<NZ, 0, MAXT>; break;
+    case 1: kern = xcorr_zwalk_zp<NZ, 1, MAXT>; break;
+    case 2: kern = xcorr_zwalk_zp<NZ, 2, MAXT>; break;
+    default: kern = xcorr_zwalk_zp<NZ, 3, MAXT>; break;
+  }
+  CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 1;
+  CT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nthr, smem));
+  const int64_t total = cdiv(a.ox, BX) * cdiv(a.oy, BY) * a.batch * a.oz;
+  const int64_t slots = (int64_t)num_sms() * std::max(1, per_sm);
+  int64_t per_cta = std::max<int64_t>(cdiv(total, slots), 2 * NZ);
+  ZRuns zr = plan_zruns(a, NZ, total / a.oz, slots);
+  if (const char* e = getenv("CT_ZW_ZC")) {  // probing only
+    per_cta = std::max(1, atoi(e));
+    zr.nc = 0;
+  }
+  const int64_t nctas = zr.nc > 0 ? (total / a.oz) * zr.nc : cdiv(total, per_cta);
+  CT_REQUIRE(nctas < (1ll << 31), "too many z-walk CTAs");
+  CUtensorMap tmap;
+  memset(&tmap, 0, sizeof(tmap));
+  if (a.sx > 256 || a.sy > 256 ||
+      !encode_tmap_4d(&tmap, a.s, sizeof(float), (uint64_t)a.mx, (uint64_t)a.my, (uint64_t)a.mz, (uint64_t)a.batch,
+                      a.sx, a.sy)) {
+    set_error("tensor map encode failed");
+    return CT_EUNSUPPORTED;
+  }
+  if (getenv("CT_DEBUG"))
+    fprintf(stderr, "xcorr_zwalk_zp NZ %d MAXT %d: tile %dx%d (%d thr) per_cta %lld runs/column %d per_sm %d ctas %lld smem %zu\n",
+            NZ, MAXT, BX, BY, nthr, (long long)per_cta, zr.nc, per_sm, (long long)nctas, smem);
+  kern<<<(unsigned)nctas, nthr, smem, st>>>(a, taps, tmap, pxa, per_cta, zr);
+  return check_launch("xcorr_zwalk_zp");
+}
+
 // Persistent 2-D variant of xcorr_pair_f32 for large kernels (config 4): a
 // CTA walks output tiles; the next tile's input values are loaded from
 // global memory into registers (PF per thread) before the current tile's
@@ -1800,6 +2123,17 @@ int launch_variant(TileArgs a, int kind, int nw, bool is3d, int txn, int tyn, co
       set_error("unsupported kernel width %d", nw);
       return CT_EUNSUPPORTED;
     }
+    if (kind == 7) {  // z-walking 3-D kernel, FFMA2 over kernel-plane pairs (fp32)
+      const int n = a.nz;
+      const float* tf = reinterpret_cast<const float*>(taps);
+      if (n == a.ny && n == nw) {
+        if (n == 3) return launch_zwalk_zp<3>(a, tf, ntaps, st);
+        if (n == 5) return launch_zwalk_zp<5>(a, tf, ntaps, st);
+        if (n == 7) return launch_zwalk_zp<7>(a, tf, ntaps, st);
+      }
+      set_error("z-walk kernel needs a 3x3x3, 5x5x5 or 7x7x7 kernel");
+      return CT_EUNSUPPORTED;
+    }
     if (kind == 5) {  // z-walking 3-D kernel with packed FFMA2 (fp32)
       const int n = a.nz;
       const float* tf = reinterpret_cast<const float*>(taps);
@@ -1930,6 +2264,7 @@ int run_tiled_autotuned(TileArgs a, int nw, bool is3d, const T* taps, int ntaps,
     choose_zwalk_tile(a.oy, a.ox, sizeof(T) == 4 ? 4 : 2, 4, a.ny, nw, &zx, &zy);
     cands.insert(cands.begin(), Variant{4, zx, zy});
     if (sizeof(T) == 4) cands.insert(cands.begin(), Variant{5, zx, zy});
+    if (sizeof(T) == 4) cands.insert(cands.begin(), Variant{7, zx, zy});
   }
   const double work = (double)a.batch * a.oz * a.oy * a.ox * (double)a.nz * a.ny * nw;
   static const bool tune = !(getenv("CT_CONV_AUTOTUNE") && atoi(getenv("CT_CONV_AUTOTUNE")) == 0);

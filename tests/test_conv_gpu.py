@@ -226,7 +226,7 @@ def test_each_kernel_variant_matches_oracle(kind, monkeypatch):
             assert rel_inf(g32[i], ref) <= 1e-5, (kind, ms, ns)
 
 
-@pytest.mark.parametrize("kind", ["0", "1", "3", "4", "5"])
+@pytest.mark.parametrize("kind", ["0", "1", "3", "4", "5", "7"])
 def test_each_3d_kernel_variant_matches_oracle(kind, monkeypatch):
     """3-D shapes with each tiled variant pinned (3 = TMA-staged z-slices, used for
     zero extension with 16-byte rows; odd rows fall back): fp64 bit-exact, fp32 1e-5."""
