@@ -610,11 +610,19 @@ __device__ __forceinline__ E warp_reduce10(const E (&o)[10], int lane, int& idx)
   return r5;
 }
 
+// CT_MOM_EARLY_REL: a warp releases frame i right after its sweep (the
+// atomic's result is consumed after the per-thread epilogue, so its latency is
+// covered and the refill is issued before the warp reduction instead of after
+// it); the combine then lags one more pair (a released frame no longer implies
+// that pair's deposit, only the previous pair's).
+#ifndef CT_MOM_EARLY_REL
+#define CT_MOM_EARLY_REL 0  // measured: no change on cfg2 (1.815 vs 1.812 ms) or 1080p fp32 (0.960 vs 0.955 ms); kept as an option
+#endif
 template <typename T, int BR, int NB, int BC, int NT>
 struct SmemWS {  // warp-streaming kernel: NB frame-band buffers + per-buffer release counters + warp partials
   static constexpr int NW = NT / 32;
-  // pair slots for the warp partials: pairs i - (NB - 1) .. i + NB - 2 can be live (see the kernel)
-  static constexpr int NS = 2 * NB - 2 > 3 ? 2 * NB - 2 : 3;
+  // pair slots for the warp partials: 2 NB pairs can be live (see the kernel)
+  static constexpr int NS = CT_MOM_EARLY_REL ? 2 * NB : (2 * NB - 2 > 3 ? 2 * NB - 2 : 3);
   static constexpr size_t buf_elems = (size_t)(BR + 1) * BC + 8;
   static constexpr size_t buf_bytes = (buf_elems * sizeof(T) + 127) & ~size_t(127);
   static constexpr size_t bars_off = NB * buf_bytes;
@@ -795,12 +803,42 @@ __device__ __forceinline__ void moments_ws_body(const MomentArgs& a, const CUten
     }
 #else
     E o[10];
+#if CT_MOM_EARLY_REL
+    // frame p0 + i (buffer i % NB) is dead for this warp once the sweep's
+    // loads have returned (the sums above depend on all of them)
+    int relv = 0;
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      relv = atomicAdd(&rel[i % NB], 1);
+    }
+#endif
     thread_sums<ACC, CPT, E, kRaw, HR>(mc, in_col, xc, yc0, o);
+#if CT_MOM_EARLY_REL
+    // the last warp to release the buffer refills it with frame p0 + i + NB
+    if (lane == 0 && (relv % NW) == NW - 1 && i + NB < nload) issue(i + NB);
+    __syncwarp();
+#endif
     int idx;
     const double wsum = (double)warp_reduce10<E>(o, lane, idx);
     double* ps = part + (size_t)(i % S::NS) * NW * 10;
     if ((lane & 1) == 0 && idx >= 0) ps[wid * 10 + idx] = wsum;
 #endif
+#if CT_MOM_EARLY_REL && !defined(CT_PROBE_NO_EPI)
+    // Pair i - NB is complete: frame i + 1 (awaited above) was loaded only
+    // after every warp released frame i + 1 - NB, i.e. finished the sweep of
+    // pair i + 1 - NB, which follows its deposit of pair i - NB.  The combine
+    // rotates over the warps: no arrival counter, no extra work on one warp.
+    if (i >= NB && wid == (i - NB) % NW) {
+      __threadfence_block();
+      combine(i - NB);
+    }
+  }
+  // the last NB pairs
+  __syncthreads();
+  for (int j = max(0, p1 - p0 - NB) + wid; j < p1 - p0; j += NW) combine(j);
+}
+#else
     // Pair i - (NB - 1) is complete: frame i + 1 (awaited above) was loaded
     // only after every warp released frame i + 1 - NB, which each warp does
     // after depositing that pair.  Its combine rotates over the warps, so no
@@ -821,6 +859,7 @@ __device__ __forceinline__ void moments_ws_body(const MomentArgs& a, const CUten
   __syncthreads();
   for (int j = max(0, p1 - p0 - (NB - 1)) + wid; j < p1 - p0; j += NW) combine(j);
 }
+#endif
 
 template <typename T, int BR, int NB, int BC, int CPT, int RS>
 __global__ void __launch_bounds__(BC / CPT * RS, ws_min_blocks<T, BC, RS>())
