@@ -57,7 +57,7 @@ struct MaxTaps<float> {
 };
 
 template <typename T>
-struct TapsParam {
+struct alignas(16) TapsParam {  // 16-byte aligned: tap rows load as 128-bit uniform loads
   T v[MaxTaps<T>::value];
 };
 
@@ -450,6 +450,9 @@ constexpr int strip_vx() {  // outputs per thread along x
   return sizeof(T) == 8 ? CT_STRIP_VX64 : 4;
 }
 
+inline void choose_tile(const TileArgs& a, int nw, int vx, int rows_per_thread, int* txn, int* tyn,
+                        bool whole_warps);  // below: threads (txn x tyn) minimising padded outputs + staging
+
 // smem bytes of xcorr_strip for these extents (0: does not fit one CTA)
 template <typename T>
 size_t strip_smem(const TileArgs& a, int nw, int txn, int tyn, int TY, bool param = false) {
@@ -472,6 +475,15 @@ int launch_strip(const TileArgs& a0, const T* k_dev, const T* taps_host, int nw,
   const int nwp = (nw + kStripC - 1) / kStripC * kStripC;
   // taps_host: the flipped taps in row-major order (nullptr: stage from k_dev)
   const bool param = taps_host != nullptr && (int64_t)a.nz * a.ny * nwp <= MaxTaps<T>::value;
+  {  // thread block shape fitted to the output extents (268^2 outputs: 25 % padded with 32 x 8 threads)
+    int tx = 32, ty = 8;
+    choose_tile(a, nwp, VX, TY, &tx, &ty, false);
+    const size_t fit = strip_smem<T>(a, nw, tx, ty, TY, param);
+    if (fit > 0 && fit <= 64 * 1024 && getenv("CT_STRIP_FIXED_TILE") == nullptr) {
+      a.txn = tx;
+      a.tyn = ty;
+    }
+  }
   const size_t smem = strip_smem<T>(a, nw, a.txn, a.tyn, TY, param);
   CT_REQUIRE(smem > 0, "kernel too large for the strip kernel");
   a.sx = a.txn * VX - VX + (VX + nwp - 1 + VX - 1) / VX * VX;
@@ -643,6 +655,157 @@ int launch_tma2d(const TileArgs& a0, const T* taps_host, int ntaps, cudaStream_t
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)num_sms() * std::max(1, per_sm)));
   kern<<<grid, a.txn * a.tyn, smem, st>>>(a, taps, tmap);
   return check_launch("xcorr_tma2d");
+}
+
+// Width-generic 2-D correlation with TMA-staged tiles: xcorr_tma2d's
+// persistent tile walk and 2-stage ring (zero extension by TMA fill, the next
+// tile in flight during the FMAs) with xcorr_strip's runtime-width compute
+// (taps in the parameter bank, strips of C compile-time taps plus one
+// compile-time tail).  Replaces the LDG-staged strip kernel where the box
+// start is 16-byte aligned: its per-tile staging (every warp waiting on its
+// global loads between two CTA barriers) was 24 % of the 13x13 fp64 kernel's
+// warp time.  Same per-output tap order: fp64 bit-identical.
+template <typename T, int C, int VX, int TY>
+__global__ void __launch_bounds__(256) xcorr_tma2d_strip(const TileArgs a, const __grid_constant__ TapsParam<T> tp,
+                                                         const __grid_constant__ CUtensorMap tmap, int nw) {
+  extern __shared__ __align__(128) unsigned char smem_tms[];
+  constexpr int VW = 16 / sizeof(T);
+  using V = typename VecT<T, VW>::type;
+  const int nwp = (nw + C - 1) / C * C;
+  const int tid = threadIdx.x;
+  const int tx = tid % a.txn, ty = tid / a.txn;
+  const int BX = a.txn * VX, BY = a.tyn * TY;
+  const int tiles_x = (a.ox + BX - 1) / BX, tiles_y = (a.oy + BY - 1) / BY;
+  const int64_t n_tiles = (int64_t)tiles_x * tiles_y * a.batch;
+  const size_t stage_bytes = ((size_t)a.sx * a.sy * sizeof(T) + 127) & ~size_t(127);
+  auto stage = [&](int s) { return reinterpret_cast<T*>(smem_tms + (size_t)s * stage_bytes); };
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_tms + 2 * stage_bytes);
+  const uint32_t box_bytes = (uint32_t)(a.sx * a.sy * sizeof(T));
+  const int ny = a.ny;
+  const int full = nw / C, tail = nw - full * C;
+  const T* taps = tp.v;
+
+  auto tile_coords = [&](int64_t t, int& x0, int& y0, int& b) {
+    b = (int)(t / ((int64_t)tiles_x * tiles_y));
+    const int r = (int)(t - (int64_t)b * tiles_x * tiles_y);
+    y0 = (r / tiles_x) * BY;
+    x0 = (r % tiles_x) * BX;
+  };
+  auto issue = [&](int64_t t, int s) {
+    int x0, y0, b;
+    tile_coords(t, x0, y0, b);
+    mbar_arrive_expect_tx(&bars[s], box_bytes);
+    tma_load_3d(stage(s), &tmap, &bars[s], x0 - a.px, y0 - a.py, b);
+  };
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  int64_t t = blockIdx.x;
+  if (tid == 0)
+    for (int k = 0; k < 2; ++k)
+      if (t + k * (int64_t)gridDim.x < n_tiles) issue(t + k * (int64_t)gridDim.x, k);
+  for (int it = 0; t < n_tiles; ++it, t += gridDim.x) {
+    const int s = it & 1;
+    mbar_wait(&bars[s], (uint32_t)((it >> 1) & 1));
+    const T* tile = stage(s);
+    T acc[1][TY][VX];
+#pragma unroll
+    for (int j = 0; j < TY; ++j)
+#pragma unroll
+      for (int r = 0; r < VX; ++r) acc[0][j][r] = T(0);
+    const int nrows = TY + ny - 1;
+    for (int r = 0; r < nrows; ++r) {
+      const T* rowp = tile + (ty * TY + r) * a.sx + tx * VX;
+      for (int st = 0; st < full; ++st)
+        strip_fma<T, C, C, VX, TY, 1>(rowp + st * C, taps + st * C, nwp, 0, r, 1, ny, acc);
+      const T* rt = rowp + full * C;
+      const T* kt_ = taps + full * C;
+      switch (tail) {  // compile-time tail strip
+#define CT_TAIL(Wt) case Wt: strip_fma<T, Wt, C, VX, TY, 1>(rt, kt_, nwp, 0, r, 1, ny, acc); break;
+        CT_TAIL(1) CT_TAIL(2) CT_TAIL(3) CT_TAIL(4) CT_TAIL(5) CT_TAIL(6) CT_TAIL(7)
+#undef CT_TAIL
+        default: break;
+      }
+    }
+    __syncthreads();  // stage s fully read: refill it with the tile two steps ahead
+    if (tid == 0 && t + 2 * (int64_t)gridDim.x < n_tiles) {
+      fence_proxy_async_smem();
+      issue(t + 2 * (int64_t)gridDim.x, s);
+    }
+    int x0, y0, b;
+    tile_coords(t, x0, y0, b);
+    T* out = reinterpret_cast<T*>(a.out) + (int64_t)b * a.oy * a.ox;
+    const int x = x0 + tx * VX;
+    const bool vec_store = (a.ox % VW == 0) && (x + VX <= a.ox);
+#pragma unroll
+    for (int yi = 0; yi < TY; ++yi) {
+      const int y = y0 + ty * TY + yi;
+      if (y >= a.oy) break;
+      T* orow = out + (int64_t)y * a.ox;
+      if (vec_store) {
+#pragma unroll
+        for (int k = 0; k < VX / VW; ++k) {
+          V q;
+          T* qp = reinterpret_cast<T*>(&q);
+#pragma unroll
+          for (int e = 0; e < VW; ++e) qp[e] = acc[0][yi][k * VW + e];
+          *reinterpret_cast<V*>(orow + x + k * VW) = q;
+        }
+      } else {
+#pragma unroll
+        for (int rr = 0; rr < VX; ++rr)
+          if (x + rr < a.ox) orow[x + rr] = acc[0][yi][rr];
+      }
+    }
+  }
+}
+
+// CT_UNSUPPORTED-free probe: can the TMA strip kernel take this problem?
+template <typename T>
+bool tma_strip_ok(const TileArgs& a, int nw, bool have_host_taps) {
+  const int nwp = (nw + kStripC - 1) / kStripC * kStripC;
+  // kernels up to ~20 x 20 taps: beyond that a tile's FMAs dwarf its staging and the second stage only
+  // costs occupancy (33x33 fp32: 0.57 ms with the ring against 0.45 ms for the LDG-staged kernel)
+  return have_host_taps && a.oz == 1 && a.nz == 1 && a.mz == 1 && a.boundary == CT_ZERO &&
+         (int64_t)a.ny * nwp <= 400 && (a.px * (int)sizeof(T)) % 16 == 0 &&
+         (a.mx * (int64_t)sizeof(T)) % 16 == 0 && (reinterpret_cast<uintptr_t>(a.s) & 15) == 0 &&
+         a.batch < (1ll << 31) && getenv("CT_CONV_NOTMA") == nullptr;
+}
+
+template <typename T, int TY>
+int launch_tma2d_strip(const TileArgs& a0, const T* taps_host, int nw, cudaStream_t st) {
+  constexpr int VX = strip_vx<T>();
+  TileArgs a = a0;
+  a.txn = 32;
+  a.tyn = 8;
+  const int nwp = (nw + kStripC - 1) / kStripC * kStripC;
+  if (getenv("CT_STRIP_FIXED_TILE") == nullptr) choose_tile(a, nwp, VX, TY, &a.txn, &a.tyn, false);
+  a.sx = a.txn * VX - VX + (VX + nwp - 1 + VX - 1) / VX * VX;
+  a.sy = a.tyn * TY + a.ny - 1;
+  const size_t stage_bytes = ((size_t)a.sx * a.sy * sizeof(T) + 127) & ~size_t(127);
+  const size_t smem = 2 * stage_bytes + 16;
+  // two stages above 64 KB cost more occupancy than the overlap returns (33x33 fp32: 0.545 vs 0.458 ms
+  // for the LDG-staged kernel): the caller falls back
+  if (a.sx > 256 || a.sy > 256 || smem > 64 * 1024) return CT_EUNSUPPORTED;
+  TapsParam<T> tp;
+  for (int row = 0; row < a.ny; ++row)
+    for (int j2 = 0; j2 < nwp; ++j2) tp.v[row * nwp + j2] = j2 < nw ? taps_host[row * nw + j2] : T(0);
+  CUtensorMap tmap;
+  memset(&tmap, 0, sizeof(tmap));
+  if (!encode_tmap_3d(&tmap, a.s, sizeof(T), (uint64_t)a.mx, (uint64_t)a.my, (uint64_t)a.batch, a.sx, a.sy))
+    return CT_EUNSUPPORTED;
+  auto kern = xcorr_tma2d_strip<T, kStripC, VX, TY>;
+  CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  CT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, a.txn * a.tyn, smem));
+  const int64_t tiles = cdiv(a.ox, a.txn * VX) * cdiv(a.oy, a.tyn * TY) * a.batch;
+  const unsigned grid =
+      (unsigned)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)num_sms() * std::max(1, per_sm)));
+  kern<<<grid, a.txn * a.tyn, smem, st>>>(a, tp, tmap, nw);
+  return check_launch("xcorr_tma2d_strip");
 }
 
 template <typename T, int LW>
@@ -2385,6 +2548,10 @@ int dispatch(int ndim, const void* s, const int64_t* ms, int64_t batch, const vo
       int rc2 = taps_to_host<T>(k, k_host, k_elems, flip, taps_h, st);
       if (rc2) return rc2;
       th = taps_h;
+    }
+    if (!is3d && tma_strip_ok<T>(a, nw, th != nullptr)) {  // TMA-staged tiles (falls through when the tile does not fit)
+      const int rc3 = launch_tma2d_strip<T, STY>(a, th, nw, st);
+      if (rc3 != CT_EUNSUPPORTED) return rc3;
     }
     if (strip_smem<T>(a, nw, 32, 8, STY, th != nullptr) > 0) {
       if (is3d) return launch_strip<T, STY, 2>(a, reinterpret_cast<const T*>(k), th, nw, flip, st);
