@@ -436,7 +436,8 @@ def secondary_configs(quick: bool, peaks):
         t = timeit(lambda: ct.direct_batch(sw, kwt, out=ow), 5)
         fl = bt * 2.0 * shp[0] * shp[1] * kw * kw
         out[name] = {"gpix_s": ow.numel() / t / 1e9, "batch": bt, "ms_per_launch": t * 1e3,
-                     "kernel": "xcorr_strip (runtime width, 8-tap strips)",
+                     "kernel": ("xcorr_tma2d_strip (runtime width, 8-tap strips, TMA-staged tiles)" if kw * kw <= 400
+                                else "xcorr_strip (runtime width, 8-tap strips)"),
                      "roofline": {"bound": "fp64" if dt == torch.float64 else "fp32", "achieved": fl / t / 1e12,
                                   "peak": pk, "unit": "TFLOP/s", "frac": fl / t / 1e12 / pk, "peak_note": pnote,
                                   "frac_vs_measured_rate": fl / t / 1e12 / mk}}
