@@ -2247,6 +2247,26 @@ inline void choose_tile(const TileArgs& a, int nw, int vx, int rows_per_thread, 
   }
 }
 
+// The K best thread blocks of choose_tile's cost model (the autotuner times them).
+inline std::vector<std::pair<int, int>> choose_tiles_top(const TileArgs& a, int nw, int vx, int rows_per_thread, int K) {
+  const double taps = (double)a.ny * (double)nw;
+  std::vector<std::pair<double, std::pair<int, int>>> all;
+  for (int tx = 4; tx <= 64; ++tx)
+    for (int ty = 1; tx * ty <= 256; ++ty) {
+      const int thr = tx * ty;
+      if (thr < 64) continue;
+      const double bx = tx * vx, by = ty * rows_per_thread;
+      const double tiles = (double)cdiv(a.ox, (int64_t)bx) * (double)cdiv(a.oy, (int64_t)by);
+      const double warp_eff = (double)thr / (double)(cdiv(thr, 32) * 32);
+      const double stage = (bx + nw + vx) * (by + a.ny - 1);
+      all.push_back({tiles * (bx * by * taps / warp_eff + 8.0 * stage), {tx, ty}});
+    }
+  std::sort(all.begin(), all.end());
+  std::vector<std::pair<int, int>> out;
+  for (size_t i = 0; i < all.size() && (int)out.size() < K; ++i) out.push_back(all[i].second);
+  return out;
+}
+
 // The tiled kernel takes its taps through the kernel-parameter bank, so they
 // are needed on the host: the caller's host copy is used when given, else the
 // device kernel is copied (a few KB, synchronising the stream).  flip
@@ -2437,7 +2457,12 @@ int run_tiled_autotuned(TileArgs a, int nw, bool is3d, const T* taps, int ntaps,
                       (a.mx * (int64_t)sizeof(T)) % 16 == 0 && (reinterpret_cast<uintptr_t>(a.s) & 15) == 0 &&
                       getenv("CT_CONV_NOTMA") == nullptr;
   if (tma_ok) {
-    for (Variant v : {Variant{2, 32, 8}, Variant{2, 16, 16}, Variant{2, 32, 4}, Variant{2, 16, 8}, Variant{2, 64, 4}}) {
+    // fixed shapes + the thread blocks fitted to the output extents (260^2 outputs: 3-9 % padded
+    // instead of 23-36 %; cfg1 0.108 -> 0.100 ms per batch of 512)
+    std::vector<Variant> tv2 = {Variant{2, 32, 8}, Variant{2, 16, 16}, Variant{2, 32, 4}, Variant{2, 16, 8},
+                                Variant{2, 64, 4}};
+    for (const auto& f : choose_tiles_top(a, nw, tma_vx<T>(), 4, 4)) tv2.push_back(Variant{2, f.first, f.second});
+    for (Variant v : tv2) {
       constexpr int tv = tma_vx<T>();
       const int sx = v.txn * tv - tv + (int)cdiv(tv + nw - 1, tv) * tv, sy = v.tyn * 4 + a.ny - 1;
       if (sx <= 256 && sy <= 256) cands.push_back(v);
@@ -2497,12 +2522,16 @@ int run_tiled_autotuned(TileArgs a, int nw, bool is3d, const T* taps, int ntaps,
     if (v.txn * v.tyn > 256 || v.txn * v.tyn < 32) continue;
     int rc = launch_variant<T>(a, v.kind, nw, is3d, v.txn, v.tyn, taps, ntaps, st);  // warm
     if (rc) continue;
-    CT_CUDA(cudaEventRecord(e0, st));
-    rc = launch_variant<T>(a, v.kind, nw, is3d, v.txn, v.tyn, taps, ntaps, st);
-    CT_CUDA(cudaEventRecord(e1, st));
-    CT_CUDA(cudaEventSynchronize(e1));
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, e0, e1);
+    float ms = 1e30f;
+    for (int rep = 0; rep < 3 && rc == CT_OK; ++rep) {  // best of three: one launch is within the box noise
+      CT_CUDA(cudaEventRecord(e0, st));
+      rc = launch_variant<T>(a, v.kind, nw, is3d, v.txn, v.tyn, taps, ntaps, st);
+      CT_CUDA(cudaEventRecord(e1, st));
+      CT_CUDA(cudaEventSynchronize(e1));
+      float t = 0.f;
+      cudaEventElapsedTime(&t, e0, e1);
+      ms = std::min(ms, t);
+    }
     if (rc == CT_OK && ms < best_ms) {
       best_ms = ms;
       best = v;
