@@ -315,3 +315,62 @@ def test_width_generic_batches_and_large_kernels():
     big = rng.standard_normal((90, 90))           # 8100 taps: shared-memory bound still fits
     t = rng.random((120, 130))
     assert np.array_equal(ct.xcorr_direct(t, big, F), O.direct(t, big, "full", flip=False))
+
+
+@pytest.mark.parametrize("kind", ["4", "7"])
+def test_zwalk_work_balanced_runs_match_flat_split_and_oracle(kind, monkeypatch):
+    """A batch large enough that the z-walk kernels cut every column into runs of
+    equal work (one run per CTA): identical bits to the flat split (the
+    per-output tap order does not depend on where a run starts) and to the
+    oracle in fp64 (kind 4); fp32 within 1e-5 (kinds 4 and 7, plane pairs)."""
+    monkeypatch.setenv("CT_CONV_KIND", kind)
+    rng = np.random.default_rng(90 + int(kind))
+    k64 = rng.standard_normal((7, 7, 7))
+    s64 = rng.random((8, 64, 96, 96))
+    for dt in (np.float32, np.float64):
+        if kind == "7" and dt is np.float64:
+            continue  # the plane-pair kernel is fp32 only
+        s, k = torch.from_numpy(s64.astype(dt)).cuda(), k64.astype(dt)
+        monkeypatch.delenv("CT_ZW_FLAT", raising=False)
+        bal = ct.direct_batch(s, k, F, flip=False).cpu().numpy()
+        monkeypatch.setenv("CT_ZW_FLAT", "1")
+        flat = ct.direct_batch(s, k, F, flip=False).cpu().numpy()
+        monkeypatch.delenv("CT_ZW_FLAT", raising=False)
+        assert np.array_equal(bal, flat), (kind, dt)
+        for i in (0, 7):
+            ref = O.direct(s64[i].astype(dt).astype(np.float64), k.astype(np.float64), "full", "zero", False)
+            if dt is np.float64:
+                assert np.array_equal(bal[i], ref), (kind, i)
+            else:
+                assert rel_inf(bal[i], ref) <= 1e-5, (kind, i)
+
+
+def test_strip_kernel_paths_agree_bit_for_bit(monkeypatch):
+    """The width-generic 2-D paths -- TMA-staged tiles with the fitted thread
+    block (default), the LDG-staged kernel (CT_CONV_NOTMA) and the fixed 32 x 8
+    block (CT_STRIP_FIXED_TILE) -- give the oracle's bits in fp64 and agree with
+    one another in fp32 (same per-output tap order on every path)."""
+    rng = np.random.default_rng(77)
+    for ms, ns, shape in [((268, 300), (13, 13), F), ((130, 257), (10, 17), S), ((96, 200), (12, 20), V),
+                          ((64, 512), (33, 33), F)]:
+        s64 = rng.random((3,) + ms)
+        k64 = rng.standard_normal(ns)
+        outs = {}
+        for name, env in (("tma", {}), ("ldg", {"CT_CONV_NOTMA": "1"}), ("fixed", {"CT_STRIP_FIXED_TILE": "1"}),
+                          ("ldg_fixed", {"CT_CONV_NOTMA": "1", "CT_STRIP_FIXED_TILE": "1"})):
+            for key in ("CT_CONV_NOTMA", "CT_STRIP_FIXED_TILE"):
+                monkeypatch.delenv(key, raising=False)
+            for key, val in env.items():
+                monkeypatch.setenv(key, val)
+            g64 = ct.direct_batch(torch.from_numpy(s64).cuda(), k64, shape, flip=True).cpu().numpy()
+            g32 = ct.direct_batch(torch.from_numpy(s64.astype(np.float32)).cuda(), k64.astype(np.float32), shape,
+                                  flip=True).cpu().numpy()
+            outs[name] = (g64, g32)
+        for key in ("CT_CONV_NOTMA", "CT_STRIP_FIXED_TILE"):
+            monkeypatch.delenv(key, raising=False)
+        for i in range(3):
+            ref = O.direct(s64[i], k64, shape.value, "zero", True)
+            for name, (g64, _) in outs.items():
+                assert np.array_equal(g64[i], ref), (name, ms, ns)
+        for name, (_, g32) in outs.items():
+            assert np.array_equal(g32, outs["tma"][1]), (name, ms, ns)
