@@ -537,16 +537,21 @@ __device__ __forceinline__ void sweep_c2d(const double* __restrict__ A, const do
 // RAW: m[6..9] are the running sums (Q2, Q3, Q5, QQ3) of a K-row sweep; with
 // Y = yc0 + K, U1 = Y S2 - Q2, U2 = Y S3 - Q3, U3 = Y S5 - Q5 and
 // U4 = Y^2 S3 - (2Y + 1) Q3 + 2 QQ3 (sweep()'s identities with the shift folded in).
-template <typename ACC, int CPT, typename E, bool RAW = false, int K = 0>
+// ALLIN: every column of every lane of the warp is inside the window (all
+// warps but a tile's first and last): no zero-initialised outputs, no
+// divergent region around the fold.
+template <typename ACC, int CPT, typename E, bool RAW = false, int K = 0, bool ALLIN = false>
 __device__ __forceinline__ void thread_sums(const ACC (&mc)[CPT][10], const bool (&in_col)[CPT],
                                             const double (&xc)[CPT], double yc0d, E (&o)[10]) {
   const E yc0 = (E)yc0d;  // centred coordinates are half-integers: exact in f32 and f64
   const E Y = yc0 + E(K);
+  if constexpr (!ALLIN || CPT > 1) {
 #pragma unroll
-  for (int q = 0; q < 10; ++q) o[q] = E(0);
+    for (int q = 0; q < 10; ++q) o[q] = E(0);
+  }
 #pragma unroll
   for (int c = 0; c < CPT; ++c) {
-    if (in_col[c]) {
+    if (ALLIN || in_col[c]) {
       const ACC(&m)[10] = mc[c];
       const E S1 = m[0], S2 = m[1], S3 = m[2], S4 = m[3], S5 = m[4], S6 = m[5];
       E U1, U2, U3, U4;
@@ -707,6 +712,10 @@ __device__ __forceinline__ void moments_ws_body(const MomentArgs& a, const CUten
     xc[c] = (double)gx - (double)(a.gw - 1) / 2.0;
   }
   const double yc0 = (double)(gy0 + r0) - (double)(a.gh - 1) / 2.0;  // centred y of this thread's first grid row
+  bool all_in_t = true;
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) all_in_t = all_in_t && in_col[c];
+  const bool all_in = __all_sync(0xffffffffu, all_in_t);  // warp-uniform: the fold without the column mask
   const int64_t row0 = (v * a.n_frames) * (int64_t)a.h + gy0;
   // thread-local row range [r_beg, r_end] (1..HR) whose grid rows are interior
   const int r_end = min(HR, a.gh - a.border - gy0 - r0);
@@ -813,7 +822,10 @@ __device__ __forceinline__ void moments_ws_body(const MomentArgs& a, const CUten
       relv = atomicAdd(&rel[i % NB], 1);
     }
 #endif
-    thread_sums<ACC, CPT, E, kRaw, HR>(mc, in_col, xc, yc0, o);
+    if (all_in)
+      thread_sums<ACC, CPT, E, kRaw, HR, true>(mc, in_col, xc, yc0, o);
+    else
+      thread_sums<ACC, CPT, E, kRaw, HR>(mc, in_col, xc, yc0, o);
 #if CT_MOM_EARLY_REL
     // the last warp to release the buffer refills it with frame p0 + i + NB
     if (lane == 0 && (relv % NW) == NW - 1 && i + NB < nload) issue(i + NB);
