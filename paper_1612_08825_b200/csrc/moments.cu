@@ -318,12 +318,37 @@ __device__ __forceinline__ void sweep_x2(const float* __restrict__ A, const floa
 // loads of one column per thread); the shifted pairs (P1, P2), (D1, D2) are
 // assembled with moves.  m[c] are column c's ten sums (same per-lane
 // operation order as sweep()).
+#ifndef CT_MOM_SCALAR_H
+#define CT_MOM_SCALAR_H 1
+#endif
 template <int BR, bool CHECK, int BC>
 __device__ __forceinline__ void sweep_c2(const float* __restrict__ A, const float* __restrict__ B, int col, int r_beg,
                                          int r_end, float (&m)[2][10]) {
   float2 s1 = {0, 0}, s2 = {0, 0}, s3 = {0, 0}, s4 = {0, 0}, s5 = {0, 0}, s6 = {0, 0};
   float2 q2 = {0, 0}, q3 = {0, 0}, q5 = {0, 0}, qq3 = {0, 0};
   float2 hP, dP, sD;
+#if CT_MOM_SCALAR_H
+  // The horizontal combinations as scalar adds written straight into the pair
+  // registers: a packed add holds the issue port as long as two scalar ones, and
+  // the shifted operand pairs (P1, P2), (D1, D2) no longer have to be assembled
+  // with moves.
+  auto row = [&](int r, float2& nhP, float2& ndP, float2& nsD) {
+    const float2 a01 = *reinterpret_cast<const float2*>(A + r * BC + col);
+    const float2 b01 = *reinterpret_cast<const float2*>(B + r * BC + col);
+    const float a2 = A[r * BC + col + 2], b2 = B[r * BC + col + 2];
+    const float2 P01 = f2add(a01, b01);
+    const float2 D01 = f2sub(b01, a01);
+    const float P2 = a2 + b2, D2 = b2 - a2;
+    nhP = make_float2(P01.x + P01.y, P01.y + P2);
+    ndP = make_float2(P01.y - P01.x, P2 - P01.y);
+    nsD = make_float2(D01.x + D01.y, D01.y + D2);
+  };
+  row(0, hP, dP, sD);
+#pragma unroll
+  for (int r = 1; r <= BR; ++r) {
+    float2 nhP, ndP, nsD;
+    row(r, nhP, ndP, nsD);
+#else
   auto row = [&](int r, float2& P01, float2& P12, float2& D01, float2& D12) {
     const float2 a01 = *reinterpret_cast<const float2*>(A + r * BC + col);
     const float2 b01 = *reinterpret_cast<const float2*>(B + r * BC + col);
@@ -345,6 +370,7 @@ __device__ __forceinline__ void sweep_c2(const float* __restrict__ A, const floa
     float2 P01, P12, D01, D12;
     row(r, P01, P12, D01, D12);
     const float2 nhP = f2add(P01, P12), ndP = f2sub(P12, P01), nsD = f2add(D01, D12);
+#endif
     if (!CHECK || (r >= r_beg && r <= r_end)) {
       const float2 ex = f2add(dP, ndP), ey = f2sub(nhP, hP), et = f2add(sD, nsD);
       s1 = f2fma(ex, ex, s1);
