@@ -399,7 +399,7 @@ def secondary_configs(quick: bool, peaks):
     s3 = torch.rand((B3, 128, 128, 128), dtype=torch.float32, device="cuda")
     k3 = np.random.Generator(np.random.PCG64(1)).standard_normal((7, 7, 7)).astype(np.float32)
     o3 = torch.empty((B3, 134, 134, 134), dtype=torch.float32, device="cuda")
-    t = timeit(lambda: ct.direct_batch(s3, k3, out=o3), 5)
+    t = timeit(lambda: ct.direct_batch(s3, k3, out=o3), 20)
     fl = B3 * 2.0 * 128 ** 3 * 343
     out["cfg3_conv3d_fp32_7^3"] = {"gpix_s": B3 * 134 ** 3 / t / 1e9, "batch": B3, "ms_per_launch": t * 1e3,
                                    "roofline": {"bound": "fp32", "achieved": fl / t / 1e12, "peak": p32,
@@ -413,7 +413,7 @@ def secondary_configs(quick: bool, peaks):
     s4 = torch.rand((B4, 2048, 2048), dtype=torch.float32, device="cuda")
     k4 = np.random.Generator(np.random.PCG64(1)).standard_normal((31, 31)).astype(np.float32)
     o4 = torch.empty((B4, 2078, 2078), dtype=torch.float32, device="cuda")
-    t = timeit(lambda: ct.direct_batch(s4, k4, out=o4), 5)
+    t = timeit(lambda: ct.direct_batch(s4, k4, out=o4), 20)
     fl = B4 * 2.0 * 2048 ** 2 * 961
     out["cfg4_conv2d_fp32_31x31"] = {"gpix_s": B4 * 2078 ** 2 / t / 1e9, "batch": B4, "ms_per_launch": t * 1e3,
                                      "roofline": {"bound": "fp32", "achieved": fl / t / 1e12, "peak": p32,
@@ -433,7 +433,7 @@ def secondary_configs(quick: bool, peaks):
         if dt == torch.float32:
             kwt = kwt.astype(np.float32)
         ow = torch.empty((bt, shp[0] + kw - 1, shp[1] + kw - 1), dtype=dt, device="cuda")
-        t = timeit(lambda: ct.direct_batch(sw, kwt, out=ow), 5)
+        t = timeit(lambda: ct.direct_batch(sw, kwt, out=ow), 20)
         fl = bt * 2.0 * shp[0] * shp[1] * kw * kw
         out[name] = {"gpix_s": ow.numel() / t / 1e9, "batch": bt, "ms_per_launch": t * 1e3,
                      "kernel": ("xcorr_tma2d_strip (runtime width, 8-tap strips, TMA-staged tiles)" if kw * kw <= 400
