@@ -845,16 +845,19 @@ struct PyrPlan {
 // level's block means, and levels 1.. run as one moments launch.
 template <typename T>
 int pyr_partials(const T* frames, int64_t nv, int nf, const PyrPlan<T>& P, char* ws, cudaStream_t st,
-                 cudaEvent_t after_l0 = nullptr) {
+                 cudaEvent_t after_l0 = nullptr, cudaStream_t st_l0 = nullptr) {
+  // st_l0 (optional): the level-0 pass runs there and `st` (blurs, levels 1.., later the epilogue) waits
+  // for it through after_l0
   const int dt = sizeof(T) == 8 ? CT_F64 : CT_F32;
   const int nl = P.nl;
   auto level = [&](int l) { return reinterpret_cast<T*>(ws + P.level_off[l]); };
   auto dec = [&](int l) { return reinterpret_cast<T*>(ws + P.dec_off[l]); };
   auto part = [&](int l) { return reinterpret_cast<double*>(ws + P.part_off[l]); };
   MomentLevel l0{frames, P.lh[0], P.lw[0], part(0), nl > 1 ? (void*)dec(1) : nullptr};
-  int rc = moments_levels_launch(dt, &l0, 1, nv, nf, 1, st);
+  int rc = moments_levels_launch(dt, &l0, 1, nv, nf, 1, st_l0 ? st_l0 : st);
   if (rc) return rc;
-  if (after_l0) CT_CUDA(cudaEventRecord(after_l0, st));
+  if (after_l0) CT_CUDA(cudaEventRecord(after_l0, st_l0 ? st_l0 : st));
+  if (st_l0 && after_l0) CT_CUDA(cudaStreamWaitEvent(st, after_l0, 0));
   for (int l = 1; l < nl; ++l) {
     rc = launch_blur_dec<T>(dec(l), nv * nf, P.lh[l - 1], P.lw[l - 1], level(l), st, l + 1 < nl ? dec(l + 1) : nullptr);
     if (rc) return rc;
@@ -875,6 +878,12 @@ int pyr_partials(const T* frames, int64_t nv, int nf, const PyrPlan<T>& P, char*
 inline int ms_parts(int64_t nv) {
   static const int env = getenv("CT_MS_PARTS") ? atoi(getenv("CT_MS_PARTS")) : 2;
   return (int)std::max<int64_t>(1, std::min<int64_t>(env, nv));
+}
+
+// CT_MS_SCHED: 0 = groups alternate over two equal-priority streams with a phase offset, 1 = priority pipeline
+inline int ms_sched() {
+  static const int env = getenv("CT_MS_SCHED") ? atoi(getenv("CT_MS_SCHED")) : 0;
+  return env;
 }
 
 template <typename T>
@@ -936,9 +945,10 @@ int run_seq(const T* frames, int64_t nv, int nf, int h, int w, int level, int ma
     return check_launch("multiscale_select");
   }
   CT_REQUIRE(nl <= kMaxPyr, "too many pyramid levels");
-  auto pipeline = [&](const T* fr, int64_t n_vid, char* w_s, double* e, cudaStream_t s, cudaEvent_t after_l0) -> int {
+  auto pipeline = [&](const T* fr, int64_t n_vid, char* w_s, double* e, cudaStream_t s, cudaEvent_t after_l0,
+                      cudaStream_t s_l0 = nullptr) -> int {
     const PyrPlan<T> P(n_vid, nf, h, w, nl);
-    int rc = pyr_partials<T>(fr, n_vid, nf, P, w_s, s, after_l0);
+    int rc = pyr_partials<T>(fr, n_vid, nf, P, w_s, s, after_l0, s_l0);
     if (rc) return rc;
     EpiLevels L;
     for (int l = 0; l < nl; ++l) {
@@ -953,6 +963,47 @@ int run_seq(const T* frames, int64_t nv, int nf, int h, int w, int level, int ma
   };
   const int parts = ms_parts(nv);
   if (parts == 1) return pipeline(frames, nv, cur, est, st, nullptr);
+  if (ms_sched() == 1) {
+    // Priority pipeline: the level-0 passes of all groups queue on a low-priority stream, everything
+    // after them (blurs, levels 1.., epilogue) on a high-priority stream, group k's tail gated on its
+    // level-0 pass and level-0 pass k + 2 on tail k (two workspace slots).  The block scheduler hands
+    // freed CTA slots to the high-priority kernels first, so a group's memory-bound tail runs beside the
+    // next group's issue-bound level-0 pass instead of after it.
+    constexpr int kMaxDevP = 64, kMaxParts = 16;
+    static thread_local cudaStream_t lo[kMaxDevP] = {}, hi[kMaxDevP] = {};
+    static thread_local cudaEvent_t ev_l0[kMaxDevP][kMaxParts] = {}, ev_done[kMaxDevP][kMaxParts] = {};
+    static thread_local cudaEvent_t ev_start[kMaxDevP] = {};
+    int dev = 0;
+    CT_CUDA(cudaGetDevice(&dev));
+    CT_REQUIRE(dev >= 0 && dev < kMaxDevP, "device index %d out of range", dev);
+    CT_REQUIRE(parts <= kMaxParts, "too many multiscale groups");
+    if (lo[dev] == nullptr) {
+      int least = 0, greatest = 0;
+      CT_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+      CT_CUDA(cudaStreamCreateWithPriority(&lo[dev], cudaStreamNonBlocking, least));
+      CT_CUDA(cudaStreamCreateWithPriority(&hi[dev], cudaStreamNonBlocking, greatest));
+      CT_CUDA(cudaEventCreateWithFlags(&ev_start[dev], cudaEventDisableTiming));
+      for (int k = 0; k < kMaxParts; ++k) {
+        CT_CUDA(cudaEventCreateWithFlags(&ev_l0[dev][k], cudaEventDisableTiming));
+        CT_CUDA(cudaEventCreateWithFlags(&ev_done[dev][k], cudaEventDisableTiming));
+      }
+    }
+    const size_t slot = align256(PyrPlan<T>((nv + parts - 1) / parts, nf, h, w, nl).total);
+    const int64_t fb = (int64_t)nf * h * w;
+    CT_CUDA(cudaEventRecord(ev_start[dev], st));
+    CT_CUDA(cudaStreamWaitEvent(lo[dev], ev_start[dev], 0));
+    CT_CUDA(cudaStreamWaitEvent(hi[dev], ev_start[dev], 0));
+    int rc = CT_OK;
+    for (int k = 0; k < parts && rc == CT_OK; ++k) {
+      const int64_t v0 = k * nv / parts, v1 = (k + 1) * nv / parts;
+      if (k >= 2) CT_CUDA(cudaStreamWaitEvent(lo[dev], ev_done[dev][k - 2], 0));  // workspace slot free again
+      rc = pipeline(frames + v0 * fb, v1 - v0, cur + (k & 1) * slot, est + v0 * (nf - 1) * 10, hi[dev],
+                    ev_l0[dev][k], lo[dev]);
+      CT_CUDA(cudaEventRecord(ev_done[dev][k], hi[dev]));
+    }
+    CT_CUDA(cudaStreamWaitEvent(st, ev_done[dev][parts - 1], 0));  // hi is in order: every group is done
+    return rc;
+  }
   // one side stream + events per (host thread, device), created once
   constexpr int kMaxDev = 64;
   static thread_local cudaStream_t sides[kMaxDev] = {};
