@@ -1271,27 +1271,6 @@ inline void choose_zwalk_tile(int oy, int ox, int vx, int ty_rows, int nh, int n
   }
 }
 
-// z-chunk length for the z-walking kernels: minimise (waves of one CTA per
-// SM) x (per-CTA time ~ zc + staging/fill overhead of the NZ-1 extra slices).
-inline int zwalk_chunk(int oz, int nz, int64_t plane_ctas, int per_sm = 1) {
-  const int64_t sms = (int64_t)num_sms() * std::max(1, per_sm);
-  int best_zc = oz;
-  double best = 1e300;
-  for (int tz = 1; tz <= oz; ++tz) {
-    const int zc = (int)cdiv(oz, tz);
-    if (tz > 1 && zc == (int)cdiv(oz, tz - 1)) continue;
-    const int64_t ctas = plane_ctas * cdiv(oz, zc);
-    if (ctas > 65535 * 64) break;
-    const double waves = (double)cdiv(ctas, sms);
-    const double cost = waves * (zc + 0.15 * (zc + nz - 1) + 2.0);
-    if (cost < best * 0.999) {
-      best = cost;
-      best_zc = zc;
-    }
-  }
-  return best_zc;
-}
-
 template <typename T, int NZ, int NH, int NW, int TY, int VX, int MAXT = 256>
 int launch_zwalk(const TileArgs& a0, const T* taps_host, int ntaps, int zc_hint, cudaStream_t st) {
   TileArgs a = a0;
