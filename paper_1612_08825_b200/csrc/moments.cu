@@ -1225,6 +1225,14 @@ size_t ws_bytes(int64_t n_videos, int n_frames, int h, int w) {
 #ifndef CT_MOM_FOUR_COL_F32
 #define CT_MOM_FOUR_COL_F32 0
 #endif
+// row groups per warp (RS): probing knob for the fp64 two-column sweep (CT_MOM_RS64=2 keeps 256 threads)
+#ifndef CT_MOM_RS64
+#define CT_MOM_RS64 1
+#endif
+template <typename T>
+constexpr int row_split() {
+  return sizeof(T) == 8 ? CT_MOM_RS64 : 1;
+}
 template <typename T, int BC>
 constexpr int cols_per_thread() {
   return (sizeof(T) == 4 && CT_MOM_FOUR_COL_F32 && BC == 256) ? 4
@@ -1280,10 +1288,11 @@ int launch_partials(const MomentArgs& a, const CUtensorMap& tmap, cudaStream_t s
   dim3 grid((unsigned)a.units, (unsigned)n_chunks, (unsigned)a.n_videos);
   static const bool sync_kernel = getenv("CT_MOM_SYNC") != nullptr;  // probing: the CTA-barrier kernel
   if (a.use_tma && !sync_kernel) {
-    using S = SmemWS<T, BR, NB, BC, BC / CPT>;
-    auto kern = ttc_moments_ws_kernel<T, BR, NB, BC, CPT, 1>;
+    constexpr int RS = row_split<T>();
+    using S = SmemWS<T, BR, NB, BC, BC / CPT * RS>;
+    auto kern = ttc_moments_ws_kernel<T, BR, NB, BC, CPT, RS>;
     CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::total));
-    kern<<<grid, BC / CPT, S::total, st>>>(a, tmap);
+    kern<<<grid, BC / CPT * RS, S::total, st>>>(a, tmap);
   } else {
     constexpr int CPS = cols_per_thread_sync<T, BC>();
     using S = Smem<T, BR, NB, BC, BC / CPS>;
@@ -1345,10 +1354,11 @@ int launch_levels_bc(const MomentLevel* lv, int n, int64_t n_videos, int n_frame
   constexpr int BR = band_rows<T>();
   constexpr int NB = ring_buffers<T>();
   constexpr int CPT = cols_per_thread<T, BC>();
-  using S = SmemWS<T, BR, NB, BC, BC / CPT>;
-  auto kern = ttc_moments_levels_kernel<T, BR, NB, BC, CPT, 1>;
+  constexpr int RS = row_split<T>();
+  using S = SmemWS<T, BR, NB, BC, BC / CPT * RS>;
+  auto kern = ttc_moments_levels_kernel<T, BR, NB, BC, CPT, RS>;
   CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::total));
-  kern<<<(unsigned)ctas, BC / CPT, S::total, st>>>(m);
+  kern<<<(unsigned)ctas, BC / CPT * RS, S::total, st>>>(m);
   return check_launch("ttc_moments_levels");
 }
 
