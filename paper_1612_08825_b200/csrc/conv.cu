@@ -523,6 +523,38 @@ int launch_strip(const TileArgs& a0, const T* k_dev, const T* taps_host, int nw,
   return check_launch("xcorr_strip");
 }
 
+// Tile walk of the persistent 2-D kernels: tile t = (image b, tile row, tile
+// column) advanced by a fixed step (the grid size) with carries instead of two
+// integer divisions per tile (the division sequences, executed by every thread
+// for the output addresses, were ~15 % of the cfg1 kernel's warp samples).
+struct TileWalk {
+  int b, ty, tx;     // current tile
+  int sb, sy, sx;    // the step in mixed radix (tiles_x, tiles_y)
+  int tiles_x, tiles_y;
+  __device__ __forceinline__ void init(int64_t t, int64_t step, int tiles_x_, int tiles_y_) {
+    tiles_x = tiles_x_;
+    tiles_y = tiles_y_;
+    const int64_t per = (int64_t)tiles_x * tiles_y;
+    b = (int)(t / per);
+    int r = (int)(t - (int64_t)b * per);
+    ty = r / tiles_x;
+    tx = r - ty * tiles_x;
+    sb = (int)(step / per);
+    r = (int)(step - (int64_t)sb * per);
+    sy = r / tiles_x;
+    sx = r - sy * tiles_x;
+  }
+  __device__ __forceinline__ void next() {
+    tx += sx;
+    const int cx = tx >= tiles_x;
+    tx -= cx ? tiles_x : 0;
+    ty += sy + cx;
+    const int cy = ty >= tiles_y;
+    ty -= cy ? tiles_y : 0;
+    b += sb + cy;
+  }
+};
+
 // ---------------------------------------------------------------------------
 // 2-D zero-extended correlation with TMA-staged tiles (the HBM-bound small-
 // kernel case, BASELINE config 1).  Persistent CTAs walk output tiles of the
@@ -560,17 +592,9 @@ __global__ void __launch_bounds__(256) xcorr_tma2d(const TileArgs a, const __gri
   const uint32_t box_bytes = (uint32_t)(a.sx * a.sy * sizeof(T));
   const int ny = a.ny;
 
-  auto tile_coords = [&](int64_t t, int& x0, int& y0, int& b) {
-    b = (int)(t / ((int64_t)tiles_x * tiles_y));
-    const int r = (int)(t - (int64_t)b * tiles_x * tiles_y);
-    y0 = (r / tiles_x) * BY;
-    x0 = (r % tiles_x) * BX;
-  };
-  auto issue = [&](int64_t t, int s) {
-    int x0, y0, b;
-    tile_coords(t, x0, y0, b);
+  auto issue = [&](const TileWalk& w, int s) {
     mbar_arrive_expect_tx(&bars[s], box_bytes);
-    tma_load_3d(stage(s), &tmap, &bars[s], x0 - a.px, y0 - a.py, b);
+    tma_load_3d(stage(s), &tmap, &bars[s], w.tx * BX - a.px, w.ty * BY - a.py, w.b);
   };
   if (tid == 0) {
     for (int k = 0; k < kTma2dStages; ++k) mbar_init(&bars[k], 1);
@@ -578,10 +602,16 @@ __global__ void __launch_bounds__(256) xcorr_tma2d(const TileArgs a, const __gri
   }
   __syncthreads();
   int64_t t = blockIdx.x;
-  if (tid == 0)
-    for (int k = 0; k < kTma2dStages; ++k)
-      if (t + k * (int64_t)gridDim.x < n_tiles) issue(t + k * (int64_t)gridDim.x, k);
-  for (int it = 0; t < n_tiles; ++it, t += gridDim.x) {
+  TileWalk cur, pre;  // the tile being computed / the tile kTma2dStages steps ahead (the refill)
+  cur.init(t, gridDim.x, tiles_x, tiles_y);
+  pre = cur;
+  for (int k = 0; k < kTma2dStages; ++k) {
+    if (tid == 0 && t + k * (int64_t)gridDim.x < n_tiles) issue(pre, k);
+    pre.next();
+  }
+  // per-thread constants of the output addressing
+  const int lx = tx * VX, ly = ty * TY;
+  for (int it = 0; t < n_tiles; ++it, t += gridDim.x, cur.next(), pre.next()) {
     const int s = it % kTma2dStages;
     mbar_wait(&bars[s], (uint32_t)((it / kTma2dStages) & 1));
     const T* tile = stage(s);
@@ -622,18 +652,15 @@ __global__ void __launch_bounds__(256) xcorr_tma2d(const TileArgs a, const __gri
     __syncthreads();  // stage s fully read: refill it with the tile kTma2dStages steps ahead
     if (tid == 0 && t + kTma2dStages * (int64_t)gridDim.x < n_tiles) {
       fence_proxy_async_smem();
-      issue(t + kTma2dStages * (int64_t)gridDim.x, s);
+      issue(pre, s);
     }
-    int x0, y0, b;
-    tile_coords(t, x0, y0, b);
-    T* out = reinterpret_cast<T*>(a.out) + (int64_t)b * a.oy * a.ox;
-    const int x = x0 + tx * VX;
+    const int x = cur.tx * BX + lx, y = cur.ty * BY + ly;
+    T* orow = reinterpret_cast<T*>(a.out) + ((int64_t)cur.b * a.oy + y) * a.ox + x;
+    const int rows = a.oy - y;  // output rows of this thread that exist (<= 0: none)
     const bool vec_store = (a.ox % VW == 0) && (x + VX <= a.ox);
 #pragma unroll
     for (int yi = 0; yi < TY; ++yi) {
-      const int y = y0 + ty * TY + yi;
-      if (y >= a.oy) break;
-      T* orow = out + (int64_t)y * a.ox;
+      if (yi >= rows) break;
       if (vec_store) {
 #pragma unroll
         for (int k = 0; k < VX / VW; ++k) {
@@ -641,13 +668,14 @@ __global__ void __launch_bounds__(256) xcorr_tma2d(const TileArgs a, const __gri
           T* qp = reinterpret_cast<T*>(&q);
 #pragma unroll
           for (int e = 0; e < VW; ++e) qp[e] = acc[yi][k * VW + e];
-          *reinterpret_cast<V*>(orow + x + k * VW) = q;
+          *reinterpret_cast<V*>(orow + k * VW) = q;
         }
       } else {
 #pragma unroll
         for (int rr = 0; rr < VX; ++rr)
-          if (x + rr < a.ox) orow[x + rr] = acc[yi][rr];
+          if (x + rr < a.ox) orow[rr] = acc[yi][rr];
       }
+      orow += a.ox;
     }
   }
 }
@@ -707,17 +735,9 @@ __global__ void __launch_bounds__(256) xcorr_tma2d_strip(const TileArgs a, const
   const int full = nw / C, tail = nw - full * C;
   const T* taps = tp.v;
 
-  auto tile_coords = [&](int64_t t, int& x0, int& y0, int& b) {
-    b = (int)(t / ((int64_t)tiles_x * tiles_y));
-    const int r = (int)(t - (int64_t)b * tiles_x * tiles_y);
-    y0 = (r / tiles_x) * BY;
-    x0 = (r % tiles_x) * BX;
-  };
-  auto issue = [&](int64_t t, int s) {
-    int x0, y0, b;
-    tile_coords(t, x0, y0, b);
+  auto issue = [&](const TileWalk& w, int s) {
     mbar_arrive_expect_tx(&bars[s], box_bytes);
-    tma_load_3d(stage(s), &tmap, &bars[s], x0 - a.px, y0 - a.py, b);
+    tma_load_3d(stage(s), &tmap, &bars[s], w.tx * BX - a.px, w.ty * BY - a.py, w.b);
   };
   if (tid == 0) {
     mbar_init(&bars[0], 1);
@@ -726,10 +746,15 @@ __global__ void __launch_bounds__(256) xcorr_tma2d_strip(const TileArgs a, const
   }
   __syncthreads();
   int64_t t = blockIdx.x;
-  if (tid == 0)
-    for (int k = 0; k < 2; ++k)
-      if (t + k * (int64_t)gridDim.x < n_tiles) issue(t + k * (int64_t)gridDim.x, k);
-  for (int it = 0; t < n_tiles; ++it, t += gridDim.x) {
+  TileWalk cur, pre;  // the tile being computed / the tile two steps ahead (the refill)
+  cur.init(t, gridDim.x, tiles_x, tiles_y);
+  pre = cur;
+  for (int k = 0; k < 2; ++k) {
+    if (tid == 0 && t + k * (int64_t)gridDim.x < n_tiles) issue(pre, k);
+    pre.next();
+  }
+  const int lx = tx * VX, ly = ty * TY;
+  for (int it = 0; t < n_tiles; ++it, t += gridDim.x, cur.next(), pre.next()) {
     const int s = it & 1;
     mbar_wait(&bars[s], (uint32_t)((it >> 1) & 1));
     const T* tile = stage(s);
@@ -767,18 +792,15 @@ __global__ void __launch_bounds__(256) xcorr_tma2d_strip(const TileArgs a, const
     __syncthreads();  // stage s fully read: refill it with the tile two steps ahead
     if (tid == 0 && t + 2 * (int64_t)gridDim.x < n_tiles) {
       fence_proxy_async_smem();
-      issue(t + 2 * (int64_t)gridDim.x, s);
+      issue(pre, s);
     }
-    int x0, y0, b;
-    tile_coords(t, x0, y0, b);
-    T* out = reinterpret_cast<T*>(a.out) + (int64_t)b * a.oy * a.ox;
-    const int x = x0 + tx * VX;
+    const int x = cur.tx * BX + lx, y = cur.ty * BY + ly;
+    T* orow = reinterpret_cast<T*>(a.out) + ((int64_t)cur.b * a.oy + y) * a.ox + x;
+    const int rows = a.oy - y;
     const bool vec_store = (a.ox % VW == 0) && (x + VX <= a.ox);
 #pragma unroll
     for (int yi = 0; yi < TY; ++yi) {
-      const int y = y0 + ty * TY + yi;
-      if (y >= a.oy) break;
-      T* orow = out + (int64_t)y * a.ox;
+      if (yi >= rows) break;
       if (vec_store) {
 #pragma unroll
         for (int k = 0; k < VX / VW; ++k) {
@@ -786,13 +808,14 @@ __global__ void __launch_bounds__(256) xcorr_tma2d_strip(const TileArgs a, const
           T* qp = reinterpret_cast<T*>(&q);
 #pragma unroll
           for (int e = 0; e < VW; ++e) qp[e] = acc[0][yi][k * VW + e];
-          *reinterpret_cast<V*>(orow + x + k * VW) = q;
+          *reinterpret_cast<V*>(orow + k * VW) = q;
         }
       } else {
 #pragma unroll
         for (int rr = 0; rr < VX; ++rr)
-          if (x + rr < a.ox) orow[x + rr] = acc[0][yi][rr];
+          if (x + rr < a.ox) orow[rr] = acc[0][yi][rr];
       }
+      orow += a.ox;
     }
   }
 }
