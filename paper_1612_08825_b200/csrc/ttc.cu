@@ -876,14 +876,15 @@ int pyr_partials(const T* frames, int64_t nv, int nf, const PyrPlan<T>& P, char*
 // Measured on 8 x 128 frames of 1080p (tools/time_cfg5.py): 1 group 4.06 us/frame, 2 groups 3.95,
 // 4 groups 3.98, 8 groups 4.11.
 inline int ms_parts(int64_t nv) {
-  static const int env = getenv("CT_MS_PARTS") ? atoi(getenv("CT_MS_PARTS")) : 2;
+  const char* e = getenv("CT_MS_PARTS");  // read per call (tests switch it)
+  const int env = e ? atoi(e) : 2;
   return (int)std::max<int64_t>(1, std::min<int64_t>(env, nv));
 }
 
 // CT_MS_SCHED: 0 = groups alternate over two equal-priority streams with a phase offset, 1 = priority pipeline
-inline int ms_sched() {
-  static const int env = getenv("CT_MS_SCHED") ? atoi(getenv("CT_MS_SCHED")) : 0;
-  return env;
+inline int ms_sched() {  // read per call (tests switch it)
+  const char* e = getenv("CT_MS_SCHED");
+  return e ? atoi(e) : 0;
 }
 
 template <typename T>

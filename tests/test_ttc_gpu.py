@@ -577,3 +577,23 @@ def test_4k_frames_multiscale_every_field():
     fin = np.isfinite(ref[:, 2]) & (ref[:, 9] == 0)
     assert np.all(np.abs(got[fin, 3] - ref[fin, 3]) <= CFG5_FOE_PX * 2 ** ref[fin, 8])
     assert np.all(np.abs(got[fin, 4] - ref[fin, 4]) <= CFG5_FOE_PX * 2 ** ref[fin, 8])
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_multiscale_group_schedules_are_bit_identical(dtype, monkeypatch):
+    """The multiscale pipeline's video groups (CT_MS_PARTS) and the way they are
+    scheduled (CT_MS_SCHED: alternating equal-priority streams, or level-0
+    passes on a low-priority stream with the tails on a high-priority one) only
+    change which launches run side by side: every video's rows are the same
+    bits as with one group."""
+    vids = np.stack([O.generate(200, 152, 6, 50.0 + 30.0 * v, (0.5, 0.5), 70 + v, 0.002) for v in range(5)])
+    dev = torch.from_numpy(vids).to(dtype).cuda()
+    monkeypatch.setenv("CT_MS_PARTS", "1")
+    monkeypatch.delenv("CT_MS_SCHED", raising=False)
+    ref = ct.run_sequence_batch(dev, max_level=3).cpu().numpy()
+    for parts, sched in (("2", "0"), ("3", "1"), ("5", "1"), ("4", "0")):
+        monkeypatch.setenv("CT_MS_PARTS", parts)
+        monkeypatch.setenv("CT_MS_SCHED", sched)
+        for _ in range(2):  # twice: the second call reuses the streams and events
+            got = ct.run_sequence_batch(dev, max_level=3).cpu().numpy()
+            assert np.array_equal(got, ref, equal_nan=True), (parts, sched)
